@@ -1,0 +1,268 @@
+"""CPU oracle of the GPU-UMAP hot path (arXiv 2008.00325) -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this module.  The product path
+(``paper_2008_00325_b200``) never imports it and shares no code with it.
+
+Wraps ``oracle/liboracle.so`` (plain C, see ``umap_oracle.c``) with numpy, plus
+the a/b curve fit (R8) done with scipy's Levenberg-Marquardt ``curve_fit`` on the
+fixed 300-point grid.  Every function cites the passage it follows; the readings
+R1..R16 are listed in DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "umap_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_c_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_c_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_c_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_c_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_I64, _I32, _F32, _F64, _U64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_double, ctypes.c_uint64
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (gcc -O2 -ffp-contract=off, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        L.oracle_philox4x32_10.argtypes = [_c_u32p, _c_u32p, _c_u32p]
+        L.oracle_philox4x32_10.restype = None
+        L.oracle_sqdist.argtypes = [_c_f32p, _c_f32p, _I32]
+        L.oracle_sqdist.restype = ctypes.c_float
+        L.oracle_knn.argtypes = [_c_f32p, _I64, _c_f32p, _I64, _I32, _I32, _I64, _c_i32p, _c_f32p]
+        L.oracle_knn.restype = ctypes.c_int
+        L.oracle_smooth_knn.argtypes = [_c_f32p, _I64, _I32, _c_f32p, _c_f32p]
+        L.oracle_membership.argtypes = [_c_f32p, _c_f32p, _c_f32p, _I64, _I32, _c_f32p]
+        L.oracle_fuzzy_union.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_i64p, _c_i32p, _c_f32p]
+        L.oracle_fuzzy_union.restype = _I64
+        L.oracle_random_init.argtypes = [_I64, _I32, _U64, _c_f32p]
+        L.oracle_edge_due.argtypes = [_F32, _I32]
+        L.oracle_edge_due.restype = ctypes.c_int
+        L.oracle_attr_coef.argtypes = [_F64, _F64, _F64]
+        L.oracle_attr_coef.restype = _F64
+        L.oracle_rep_coef.argtypes = [_F64, _F64, _F64, _F64]
+        L.oracle_rep_coef.restype = _F64
+        L.oracle_optimize.argtypes = [_c_i64p, _c_i32p, _c_f32p, _I64, _I32, _c_f32p, _F32, _F32, _F32, _F32,
+                                      _I32, _I32, _I32, _I32, _U64, _I32]
+        L.oracle_transform_init.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_f32p, _I32, _c_f32p]
+        L.oracle_transform_optimize.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_f32p, _I64, _I32, _c_f32p,
+                                                _F32, _F32, _F32, _F32, _I32, _I32, _U64, _I64]
+        L.oracle_trust_penalty.argtypes = [_c_f32p, _I32, _c_f32p, _I32, _I64, _I32, _I64, _I64,
+                                           ctypes.c_void_p]
+        L.oracle_trust_penalty.restype = _I64
+        L.oracle_trust_from_penalty.argtypes = [_I64, _I64, _I32]
+        L.oracle_trust_from_penalty.restype = _F64
+        _lib = L
+    return _lib
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ---------------------------------------------------------------- Philox (R11)
+def philox4x32_10(ctr, key):
+    out = np.zeros(4, np.uint32)
+    lib().oracle_philox4x32_10(np.asarray(ctr, np.uint32), np.asarray(key, np.uint32), out)
+    return out
+
+
+# ------------------------------------------------------------ kNN (R1, R2)
+def sqdist(x, y) -> float:
+    x, y = _f32(x), _f32(y)
+    return float(lib().oracle_sqdist(x, y, x.shape[0]))
+
+
+def knn(Xq, Xr, k: int, self_offset: int = -1):
+    """Exact kNN by key (fp32 sequential-FMA d^2, index). Returns (idx int32, dist fp32)."""
+    Xq, Xr = _f32(Xq), _f32(Xr)
+    nq, d = Xq.shape
+    idx = np.empty((nq, k), np.int32)
+    dist = np.empty((nq, k), np.float32)
+    lib().oracle_knn(Xq, nq, Xr, Xr.shape[0], d, k, self_offset, idx, dist)
+    return idx, dist
+
+
+# ----------------------------------------------------- rho, sigma, w (R4-R6)
+def smooth_knn(dist):
+    """Eq. 1: per-row rho and sigma."""
+    dist = _f32(dist)
+    n, k = dist.shape
+    rho = np.empty(n, np.float32)
+    sigma = np.empty(n, np.float32)
+    lib().oracle_smooth_knn(dist, n, k, rho, sigma)
+    return rho, sigma
+
+
+def membership(dist, rho, sigma):
+    """w_ij = exp(-max(0, d_ij - rho_i)/sigma_i)."""
+    dist = _f32(dist)
+    n, k = dist.shape
+    w = np.empty((n, k), np.float32)
+    lib().oracle_membership(dist, _f32(rho), _f32(sigma), n, k, w)
+    return w
+
+
+# ------------------------------------------------------------ union (R7)
+def fuzzy_union(idx, w):
+    """Eq. 2: B = A + A^T - A o A^T as CSR sorted by (row, col)."""
+    idx = np.ascontiguousarray(idx, np.int32)
+    w = _f32(w)
+    n, k = idx.shape
+    indptr = np.zeros(n + 1, np.int64)
+    col = np.empty(2 * n * k, np.int32)
+    val = np.empty(2 * n * k, np.float32)
+    nnz = lib().oracle_fuzzy_union(idx, w, n, k, indptr, col, val)
+    return indptr, col[:nnz].copy(), val[:nnz].copy()
+
+
+# ------------------------------------------------------------ a, b (R8)
+def fit_ab(min_dist: float = 0.1, spread: float = 1.0):
+    """Fit Phi(d) = 1/(1 + a d^{2b}) (Eq. 3's "approximate form") to the
+    min_dist curve y = 1 (x < min_dist), exp(-(x - min_dist)/spread) otherwise, on
+    linspace(0, 3*spread, 300), by Levenberg-Marquardt from (1, 1)."""
+    from scipy.optimize import curve_fit
+
+    def curve(x, a, b):
+        return 1.0 / (1.0 + a * x ** (2 * b))
+
+    xv = np.linspace(0, spread * 3, 300)
+    yv = np.zeros(xv.shape)
+    yv[xv < min_dist] = 1.0
+    yv[xv >= min_dist] = np.exp(-(xv[xv >= min_dist] - min_dist) / spread)
+    params, _ = curve_fit(curve, xv, yv)
+    return float(params[0]), float(params[1])
+
+
+# ------------------------------------------------------------ SGD (R9-R14)
+def random_init(n: int, dim: int, seed: int):
+    Y = np.empty((n, dim), np.float32)
+    lib().oracle_random_init(n, dim, seed, Y)
+    return Y
+
+
+def edge_due(r: float, e: int) -> bool:
+    return bool(lib().oracle_edge_due(np.float32(r), e))
+
+
+def attr_coef(s, a, b):
+    return lib().oracle_attr_coef(s, a, b)
+
+
+def rep_coef(s, a, b, gamma=1.0):
+    return lib().oracle_rep_coef(s, a, b, gamma)
+
+
+def optimize(indptr, col, w, Y, a, b, n_epochs, e_begin=1, e_end=None, m=5, seed=0,
+             mode="deterministic", gamma=1.0, alpha0=1.0):
+    """SGD layout over the union. Returns a new Y (input not modified)."""
+    Y = np.array(Y, dtype=np.float32, order="C", copy=True)
+    n, dim = Y.shape
+    if e_end is None:
+        e_end = n_epochs
+    lib().oracle_optimize(np.ascontiguousarray(indptr, np.int64), np.ascontiguousarray(col, np.int32),
+                          _f32(w), n, dim, Y, a, b, gamma, alpha0, n_epochs, e_begin, e_end, m, seed,
+                          1 if mode == "deterministic" else 0)
+    return Y
+
+
+def transform_init(idx, w, Ytr):
+    idx = np.ascontiguousarray(idx, np.int32)
+    nq, k = idx.shape
+    Ytr = _f32(Ytr)
+    Yq = np.empty((nq, Ytr.shape[1]), np.float32)
+    lib().oracle_transform_init(idx, _f32(w), nq, k, Ytr, Ytr.shape[1], Yq)
+    return Yq
+
+
+def transform_optimize(idx, w, Ytr, Yq, a, b, n_epochs_t, m=5, seed=0, q_offset=0, gamma=1.0, alpha0=1.0):
+    idx = np.ascontiguousarray(idx, np.int32)
+    nq, k = idx.shape
+    Ytr = _f32(Ytr)
+    Yq = np.array(Yq, dtype=np.float32, order="C", copy=True)
+    lib().oracle_transform_optimize(idx, _f32(w), nq, k, Ytr, Ytr.shape[0], Ytr.shape[1], Yq, a, b, gamma,
+                                    alpha0, n_epochs_t, m, seed, q_offset)
+    return Yq
+
+
+# ------------------------------------------------------------ trust (R16)
+def trust_penalty(X, Y, k, row_begin=0, row_end=None):
+    X, Y = _f32(X), _f32(Y)
+    n = X.shape[0]
+    if row_end is None:
+        row_end = n
+    pen = np.zeros(row_end - row_begin, np.int64)
+    S = lib().oracle_trust_penalty(X, X.shape[1], Y, Y.shape[1], n, k, row_begin, row_end,
+                                   pen.ctypes.data_as(ctypes.c_void_p))
+    return int(S), pen
+
+
+def trust_from_penalty(S, n, k):
+    return float(lib().oracle_trust_from_penalty(S, n, k))
+
+
+def trustworthiness(X, Y, k):
+    S, _ = trust_penalty(X, Y, k)
+    return trust_from_penalty(S, X.shape[0], k)
+
+
+# ------------------------------------------------------------ pipelines
+DEFAULTS = dict(k=15, n_components=2, min_dist=0.1, spread=1.0, m=5, gamma=1.0, alpha0=1.0)
+
+
+def default_epochs(n):
+    """500 epochs when n <= 10000 else 200."""
+    return 500 if n <= 10000 else 200
+
+
+def fuzzy_graph(X, k):
+    idx, dist = knn(X, X, k, self_offset=0)
+    rho, sigma = smooth_knn(dist)
+    w = membership(dist, rho, sigma)
+    return idx, dist, rho, sigma, w, fuzzy_union(idx, w)
+
+
+def fit(X, k=15, n_components=2, n_epochs=None, a=None, b=None, min_dist=0.1, spread=1.0, m=5, seed=0,
+        mode="deterministic"):
+    """Whole fit: kNN -> rho/sigma -> membership -> union -> init -> SGD."""
+    X = _f32(X)
+    n = X.shape[0]
+    if n_epochs is None:
+        n_epochs = default_epochs(n)
+    if a is None or b is None:
+        a, b = fit_ab(min_dist, spread)
+    _, _, _, _, _, (indptr, col, w) = fuzzy_graph(X, k)
+    Y0 = random_init(n, n_components, seed)
+    return optimize(indptr, col, w, Y0, np.float32(a), np.float32(b), n_epochs, m=m, seed=seed, mode=mode)
+
+
+def transform(X_train, Y_train, Xq, k=15, n_epochs=200, a=None, b=None, m=5, seed=0, q_offset=0):
+    """Out-of-sample embedding against the frozen training layout."""
+    if a is None or b is None:
+        a, b = fit_ab()
+    idx, dist = knn(Xq, X_train, k, self_offset=-1)
+    rho, sigma = smooth_knn(dist)
+    w = membership(dist, rho, sigma)
+    Yq = transform_init(idx, w, Y_train)
+    n_t = int(math.ceil(n_epochs / 3.0))
+    return transform_optimize(idx, w, Y_train, Yq, np.float32(a), np.float32(b), n_t, m=m, seed=seed,
+                              q_offset=q_offset)
