@@ -1,0 +1,223 @@
+/*
+ * umap_b200.h -- C ABI of the B200-native GPU-UMAP hot path (arXiv 2008.00325).
+ *
+ * Paper: "Faster, Simpler and More Accurate: GPU-accelerated UMAP"
+ * (PAPER.md, cited P:<line>).  Readings of garbled / silent passages are
+ * R1..R16 in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", plain pointers and sizes; no C++ or torch types.
+ *  - Layout: every matrix is row-major, C-contiguous (X: n x d fp32, row i at
+ *    X + i*d; Y: n x n_components fp32).  Index arrays are int32 unless named
+ *    indptr (int64).
+ *  - Pointers: the top-level calls umap_fit, umap_transform and
+ *    umap_trustworthiness accept HOST or DEVICE pointers for every array (the
+ *    kind is detected with cudaPointerGetAttributes; host arrays are staged
+ *    through the device inside the call).  All building-block calls take
+ *    DEVICE pointers only and return UMAP_ERR_NOT_DEVICE_POINTER otherwise.
+ *  - Ownership: the caller owns every buffer.  Inputs are read-only and not
+ *    retained after return; outputs are caller-allocated with the documented
+ *    shape.  Scratch is allocated stream-ordered (cudaMallocAsync on `stream`,
+ *    the analogue of the paper's RMM pool) and freed before return.
+ *  - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Work
+ *    is enqueued on it and every call returns after that work completed.
+ *  - Errors: a umap_status code.  Nothing throws across the ABI or aborts.
+ *    Outputs are unspecified on error.  umap_last_error() gives a thread-local
+ *    detail string.
+ *  - The library never falls back to the CPU: without a CUDA device every
+ *    compute call returns UMAP_ERR_CUDA.
+ */
+#ifndef UMAP_B200_H
+#define UMAP_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define UMAP_API __attribute__((visibility("default")))
+#else
+#define UMAP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    UMAP_OK = 0,
+    UMAP_ERR_INVALID_ARGUMENT = 1,
+    UMAP_ERR_NOT_DEVICE_POINTER = 2,
+    UMAP_ERR_TOO_FEW_ROWS = 3,
+    UMAP_ERR_K_OUT_OF_RANGE = 4,
+    UMAP_ERR_NONFINITE_INPUT = 5,
+    UMAP_ERR_NONFINITE_EMBEDDING = 6,
+    UMAP_ERR_FIT_AB_NO_CONVERGENCE = 7,
+    UMAP_ERR_CUDA = 8,
+    UMAP_ERR_OUT_OF_MEMORY = 9,
+    UMAP_ERR_UNSUPPORTED = 10
+} umap_status;
+
+/* SGD layout mode. */
+typedef enum {
+    UMAP_SGD_HOGWILD = 0,       /* racy in-place push updates with fp32 atomics */
+    UMAP_SGD_DETERMINISTIC = 1  /* epoch-buffered updates, bit-reproducible (R13)   */
+} umap_sgd_mode;
+
+/* kNN distance mode. */
+typedef enum {
+    UMAP_KNN_EXACT_FP32 = 0,    /* exact fp32 distances, sequential FMA per feature (R2)   */
+    UMAP_KNN_TENSOR_BF16 = 1    /* tcgen05 BF16 candidate GEMM + exact fp32 re-rank (R3)   */
+} umap_knn_mode;
+
+typedef struct {
+    uint32_t struct_size;          /* = sizeof(umap_params); ABI versioning                 */
+    int32_t  n_neighbors;          /* k (P:232 default 15); 2 <= k < n, k <= 64              */
+    int32_t  n_components;         /* embedding dimension: 1..4, 8 or 16 (default 2)         */
+    int32_t  n_epochs;             /* N; 0 -> 500 if n <= 10000 else 200                     */
+    float    min_dist;             /* Eq. 3, default 0.1                           */
+    float    spread;               /* default 1.0                                           */
+    int32_t  negative_sample_rate; /* m negatives per positive edge, default 5        */
+    float    learning_rate;        /* alpha0, default 1.0 (decays linearly, R10)             */
+    float    repulsion_strength;   /* gamma, default 1.0                                    */
+    float    a, b;                 /* Phi(d) = 1/(1 + a d^{2b}); 0,0 -> fitted (umap_fit_ab) */
+    uint64_t seed;                 /* Philox key for init and negative sampling      */
+    int32_t  sgd_mode;             /* umap_sgd_mode, default UMAP_SGD_DETERMINISTIC          */
+    int32_t  knn_mode;             /* umap_knn_mode, default UMAP_KNN_EXACT_FP32             */
+    int32_t  knn_candidates;       /* k' candidates per row before re-rank (TC mode), 32     */
+    int32_t  transform_epochs;     /* 0 -> ceil(n_epochs / 3) (R15)                          */
+} umap_params;
+
+/* Per-stage device times (ms, CUDA events on `stream`) and graph statistics. */
+typedef struct {
+    double  ms_knn, ms_smooth, ms_union, ms_init, ms_sgd, ms_total;
+    int64_t nnz;            /* entries of the fuzzy union B (both directions)              */
+    int64_t positives;      /* sum over epochs of due directed edges (edge-updates)        */
+    float   w_max;          /* max weight of B (1.0 on every non-empty graph)              */
+    float   a, b;           /* curve parameters used                                       */
+    int32_t n_epochs;       /* N used                                                      */
+    int32_t gpu_launches;   /* kernels launched by this call                               */
+} umap_fit_stats;
+
+/* Fill *p with the defaults above. */
+UMAP_API void umap_params_default(umap_params* p);
+
+/* R8: least-squares fit of Phi(x) = 1/(1 + a x^{2b}) to y(x) = 1 (x < min_dist),
+ * exp(-(x - min_dist)/spread) otherwise, on 300 points of [0, 3 spread]
+ * (Eq. 3's "approximate form").  Host only; no CUDA needed.
+ * Errors: INVALID_ARGUMENT (spread <= 0, min_dist < 0), FIT_AB_NO_CONVERGENCE. */
+UMAP_API umap_status umap_fit_ab(float min_dist, float spread, float* a, float* b);
+
+/* Whole fit: kNN (a2) -> rho/sigma + membership (a3, a4) ->
+ * fuzzy union (a5) -> random init (a7) -> SGD layout (a6, a8).
+ * X: n x d fp32 (host or device); Y: n x n_components fp32 output (host or device).
+ * stats: optional (NULL), host memory.
+ * Errors: TOO_FEW_ROWS (n <= k), K_OUT_OF_RANGE, NONFINITE_INPUT, NONFINITE_EMBEDDING,
+ * UNSUPPORTED (n_components not in {1,2,3,4,8,16}), CUDA, OUT_OF_MEMORY. */
+UMAP_API umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_params* p,
+                     float* Y, umap_fit_stats* stats, void* stream);
+
+/* f1 pre-computed kNN graph ("accept a k-NN graph that has already been
+ * computed", App. A.1): the fit from a3 on.  knn_idx n x k int32 (global ids,
+ * self excluded), knn_dist n x k fp32, each row sorted ascending (umap_knn output);
+ * k = p->n_neighbors.  Host or device pointers.  Same outputs and errors as umap_fit. */
+UMAP_API umap_status umap_fit_knn(const int32_t* knn_idx, const float* knn_dist, int64_t n, const umap_params* p,
+                                  float* Y, umap_fit_stats* stats, void* stream);
+
+/* Out-of-sample embedding against a frozen training layout (R15):
+ * kNN of X_q against X_train (no self exclusion), rho/sigma/membership on the
+ * query rows, init = weighted mean of the neighbours' Y_train (L1 row
+ * normalisation), then transform_epochs epochs of SGD moving only the
+ * query rows, negatives drawn from the training rows.
+ * q_offset: global index of X_q's first row; it keys the RNG so a partitioned
+ * run equals the single run bit for bit.
+ * X_train n_train x d, Y_train n_train x n_components, X_q n_q x d, Y_q n_q x n_components. */
+UMAP_API umap_status umap_transform(const float* X_train, const float* Y_train, int64_t n_train, int32_t d,
+                           const float* X_q, int64_t n_q, int64_t q_offset, const umap_params* p,
+                           float* Y_q, void* stream);
+
+/* Trustworthiness T(k) (Alg. 1, R16):
+ * T = 1 - 2/(n k (2n - 3k - 1)) * sum_i sum_{j in NN_k(Y_i)} max(0, r_i(j) - k),
+ * r_i(j) = 1 + #{l != i : (d2_X(i,l), l) < (d2_X(i,j), j)}.
+ * X n x d, Y n x d_emb (host or device); T (host double), penalty (host int64,
+ * optional NULL) = the integer sum.  Requires 1 <= k < n/2.
+ * knn_mode: UMAP_KNN_EXACT_FP32 (only mode in this build; TENSOR -> UNSUPPORTED). */
+UMAP_API umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int32_t d_emb, int64_t n,
+                                 int32_t k, int32_t knn_mode, double* T, int64_t* penalty, void* stream);
+
+/* ---------------- building blocks (DEVICE pointers only) ---------------- */
+
+/* a2 kNN (R1, R2): for each query row i, the k reference rows with smallest key
+ * (d2, global id), d2 = fp32 sum over f ascending of fmaf(t, t, s), t = xq_if - xr_jf.
+ * Global ids: query row i is point query_offset + i, reference row j is point
+ * index_offset + j (the shard offset of a sharded kNN, 8(e)); keys and output ids use
+ * global reference ids.  exclude_self != 0 drops the reference row whose global id
+ * equals the query's own (R1: "k true neighbours", self excluded by index).
+ * idx: n_q x k int32, dist: n_q x k fp32 = sqrtf(d2) (or d2 itself when out_squared != 0),
+ * rows sorted ascending by key.  Requires 1 <= k <= 64, k <= n_r - (exclude_self != 0).
+ * knn_mode TENSOR_BF16: candidates by a tcgen05 BF16 GEMM, re-ranked exactly (R3). */
+UMAP_API umap_status umap_knn(const float* X_q, int64_t n_q, const float* X_r, int64_t n_r, int32_t d, int32_t k,
+                     int64_t query_offset, int64_t index_offset, int32_t exclude_self, int32_t knn_mode,
+                     int32_t out_squared,
+                     int32_t* idx, float* dist, void* stream);
+
+/* Merge n_parts per-part candidate lists (part-major: idx_in[p][n][k_in], d2_in likewise,
+ * each row sorted by key) into the k_out smallest keys (d2, id).  dist = sqrtf(d2)
+ * (out_squared = 0) or d2.  Used by the sharded kNN (NCCL all-gather, 8(e)). */
+UMAP_API umap_status umap_topk_merge(const int32_t* idx_in, const float* d2_in, int32_t n_parts, int64_t n,
+                            int32_t k_in, int32_t k_out, int32_t out_squared, int32_t* idx, float* dist,
+                            void* stream);
+
+/* a3 + a4 (Eq. 1; R4-R6): per row rho, sigma (fp64 bisection)
+ * and memberships w (n x k).  dist: n x k fp32 sorted ascending.  rho, sigma: n fp32
+ * (either may be NULL).  If col_sorted_idx != NULL, each row of (idx, w) is also written
+ * re-ordered by ascending column id into col_sorted_idx / w (the union's input);
+ * otherwise w keeps the distance order. */
+UMAP_API umap_status umap_smooth_knn(const float* dist, const int32_t* idx, int64_t n, int32_t k,
+                            float* rho, float* sigma, float* w, int32_t* col_sorted_idx, void* stream);
+
+/* a5 fuzzy union (Eq. 2; R7): B = A + A^T - A o A^T, zeros dropped,
+ * CSR sorted by (row, col).  idx/w: n x k, rows sorted by column (umap_smooth_knn
+ * col_sorted_idx output).  indptr: n+1 int64; col, val: capacity entries
+ * (2 n k always suffices).  *nnz (host) receives the number of entries. */
+UMAP_API umap_status umap_fuzzy_union(const int32_t* idx, const float* w, int64_t n, int32_t k,
+                             int64_t* indptr, int32_t* col, float* val, int64_t capacity,
+                             int64_t* nnz, void* stream);
+
+/* a7 random init (R11): Y[v][c] = -10 + 20 (u >> 8) 2^-24,
+ * u = Philox4x32-10(key = seed, ctr = (v, c, 0xFFFFFFFF, 0))[0]. */
+UMAP_API umap_status umap_random_init(int64_t n, int32_t dim, uint64_t seed, float* Y, void* stream);
+
+/* a6 + a8 SGD layout over the union B (CSR from umap_fuzzy_union), epochs
+ * e_begin..e_end-1 of an N = p->n_epochs schedule (R9-R14), Y (n x n_components) in place.
+ * Uses p->a, p->b (must be > 0), gamma, alpha0, m, seed, sgd_mode.
+ * positives (host, optional) receives the number of due directed edges processed. */
+UMAP_API umap_status umap_optimize(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                          float* Y, const umap_params* p, int32_t e_begin, int32_t e_end,
+                          int64_t* positives, void* stream);
+
+/* a9 transform SGD stage (R15): query graph idx/w (n_q x k, distance order),
+ * Y_q in/out (n_q x n_components), Y_train frozen.  Epochs e_begin..e_end-1 of an
+ * N_t = n_epochs_t schedule.  init != 0: first set Y_q to the weighted mean of the
+ * neighbours' Y_train. */
+UMAP_API umap_status umap_transform_optimize(const int32_t* idx, const float* w, int64_t n_q, int32_t k,
+                                    const float* Y_train, int64_t n_train, float* Y_q,
+                                    const umap_params* p, int32_t n_epochs_t, int32_t e_begin,
+                                    int32_t e_end, int64_t q_offset, int32_t init, void* stream);
+
+/* a10 input-space rank penalties for rows [row_begin, row_end) (R16): emb_idx is the
+ * embedding kNN of those rows (n_rows x k, global ids).  row_pen: n_rows int64
+ * (optional NULL); *penalty (host) = sum. */
+UMAP_API umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
+                               int64_t row_begin, int64_t row_end, int64_t* row_pen, int64_t* penalty,
+                               void* stream);
+
+UMAP_API const char* umap_status_string(umap_status s);
+UMAP_API const char* umap_last_error(void);
+/* Number of this library's kernels launched by the calling thread since load. */
+UMAP_API int64_t     umap_kernel_launch_count(void);
+/* Library version string. */
+UMAP_API const char* umap_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UMAP_B200_H */

@@ -66,6 +66,8 @@ def lib():
         L.oracle_transform_init.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_f32p, _I32, _c_f32p]
         L.oracle_transform_optimize.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_f32p, _I64, _I32, _c_f32p,
                                                 _F32, _F32, _F32, _F32, _I32, _I32, _U64, _I64]
+        L.oracle_transform_optimize_range.argtypes = [_c_i32p, _c_f32p, _I64, _I32, _c_f32p, _I64, _I32, _c_f32p,
+                                                      _F32, _F32, _F32, _F32, _I32, _I32, _I32, _I32, _U64, _I64]
         L.oracle_trust_penalty.argtypes = [_c_f32p, _I32, _c_f32p, _I32, _I64, _I32, _I64, _I64,
                                            ctypes.c_void_p]
         L.oracle_trust_penalty.restype = _I64
@@ -194,13 +196,17 @@ def transform_init(idx, w, Ytr):
     return Yq
 
 
-def transform_optimize(idx, w, Ytr, Yq, a, b, n_epochs_t, m=5, seed=0, q_offset=0, gamma=1.0, alpha0=1.0):
+def transform_optimize(idx, w, Ytr, Yq, a, b, n_epochs_t, m=5, seed=0, q_offset=0, gamma=1.0, alpha0=1.0,
+                       e_begin=1, e_end=None):
+    """Query-row SGD, epochs [e_begin, e_end) of an N_t = n_epochs_t schedule."""
     idx = np.ascontiguousarray(idx, np.int32)
     nq, k = idx.shape
     Ytr = _f32(Ytr)
     Yq = np.array(Yq, dtype=np.float32, order="C", copy=True)
-    lib().oracle_transform_optimize(idx, _f32(w), nq, k, Ytr, Ytr.shape[0], Ytr.shape[1], Yq, a, b, gamma,
-                                    alpha0, n_epochs_t, m, seed, q_offset)
+    if e_end is None:
+        e_end = n_epochs_t
+    lib().oracle_transform_optimize_range(idx, _f32(w), nq, k, Ytr, Ytr.shape[0], Ytr.shape[1], Yq, a, b, gamma,
+                                          alpha0, n_epochs_t, e_begin, e_end, m, seed, q_offset)
     return Yq
 
 

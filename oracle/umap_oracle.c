@@ -396,16 +396,18 @@ int oracle_transform_init(const int32_t* idx, const float* w, int64_t nq, int32_
 /* query graph.  RNG counter uses the GLOBAL query id (q + q_offset) so a    */
 /* partitioned run equals the single run.  In place, fp64        */
 /* arithmetic, fp32 storage.                                                */
-int oracle_transform_optimize(const int32_t* idx, const float* w, int64_t nq, int32_t k,
-                              const float* Ytr, int64_t ntr, int32_t dim, float* Yq,
-                              float a, float b, float gamma, float alpha0, int32_t n_epochs_t,
-                              int32_t m, uint64_t seed, int64_t q_offset)
+int oracle_transform_optimize_range(const int32_t* idx, const float* w, int64_t nq, int32_t k,
+                                    const float* Ytr, int64_t ntr, int32_t dim, float* Yq,
+                                    float a, float b, float gamma, float alpha0, int32_t n_epochs_t,
+                                    int32_t e_begin, int32_t e_end, int32_t m, uint64_t seed, int64_t q_offset)
 {
     float w_max = 0.0f;
     for (int64_t p = 0; p < nq * k; ++p) if (w[p] > w_max) w_max = w[p];
     if (w_max <= 0.0f) return 0;
     double* g = (double*)malloc(sizeof(double) * (size_t)dim);
-    for (int32_t e = 1; e < n_epochs_t; ++e) {
+    if (e_begin < 1) e_begin = 1;
+    if (e_end > n_epochs_t) e_end = n_epochs_t;
+    for (int32_t e = e_begin; e < e_end; ++e) {
         float alpha = alpha0 * (1.0f - (float)e / (float)n_epochs_t);
         for (int64_t q = 0; q < nq; ++q) {
             float* yq = Yq + q * dim;
@@ -442,6 +444,15 @@ int oracle_transform_optimize(const int32_t* idx, const float* w, int64_t nq, in
     }
     free(g);
     return 0;
+}
+
+int oracle_transform_optimize(const int32_t* idx, const float* w, int64_t nq, int32_t k,
+                              const float* Ytr, int64_t ntr, int32_t dim, float* Yq,
+                              float a, float b, float gamma, float alpha0, int32_t n_epochs_t,
+                              int32_t m, uint64_t seed, int64_t q_offset)
+{
+    return oracle_transform_optimize_range(idx, w, nq, k, Ytr, ntr, dim, Yq, a, b, gamma, alpha0, n_epochs_t,
+                                           1, n_epochs_t, m, seed, q_offset);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -1,0 +1,660 @@
+// api.cu -- the C ABI (include/umap_b200.h): validation, host/device staging,
+// the fit / transform / trustworthiness pipelines and the host-side a,b fit.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace umapb200 {
+
+// ---- kernels / stage drivers from the other translation units
+umap_status knn_exact(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int64_t self_shift,
+                      int exclude_self, int64_t index_offset, int out_squared, int32_t* idx, float* dist,
+                      cudaStream_t s);
+umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
+                       int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
+                       float* dist, cudaStream_t s);
+umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
+                       int out_squared, int32_t* idx, float* dist, cudaStream_t s);
+umap_status smooth_knn(const float* dist, const int32_t* idx, int64_t n, int k, float* rho, float* sigma, float* w,
+                       int32_t* col_sorted, cudaStream_t s);
+umap_status fuzzy_union(const int32_t* acol, const float* aw, int64_t n, int k, int64_t* indptr, int32_t* col,
+                        float* val, int64_t capacity, int64_t* nnz_host, cudaStream_t s);
+umap_status random_init(int64_t n, int dim, uint64_t seed, float* Y, cudaStream_t s);
+umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const float* val, int64_t n, int64_t nnz,
+                            float* Y, const umap_params* p, int e_begin, int e_end, int64_t* positives_host,
+                            cudaStream_t s);
+umap_status transform_optimize(const int32_t* idx, const float* w, int64_t nq, int k, const float* Ytr, int64_t ntr,
+                               float* Yq, const umap_params* p, int n_epochs_t, int e_begin, int e_end,
+                               int64_t q_offset, int init, cudaStream_t s);
+umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, cudaStream_t s);
+bool dim_supported(int dim);
+
+// ---- error state
+static thread_local std::string g_last_error;
+static thread_local int64_t g_launches = 0;
+
+void set_last_error(const std::string& s) { g_last_error = s; }
+void count_launch(int n) { g_launches += n; }
+
+umap_status cuda_status(cudaError_t e, const char* what)
+{
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    cudaGetLastError();  // clear sticky-free errors
+    return e == cudaErrorMemoryAllocation ? UMAP_ERR_OUT_OF_MEMORY : UMAP_ERR_CUDA;
+}
+
+namespace {
+
+__global__ void nonfinite_kernel(const float* __restrict__ x, int64_t m, int* __restrict__ flag)
+{
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+umap_status any_nonfinite(const float* x, int64_t m, bool* out, cudaStream_t s)
+{
+    Scratch flag;
+    UMAP_TRY(flag.alloc(sizeof(int), s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+    if (m > 0) {
+        const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(m, 256), 8LL * num_sms());
+        nonfinite_kernel<<<grid, 256, 0, s>>>(x, m, flag.as<int>());
+        UMAP_LAUNCH_CHECK("nonfinite_kernel");
+    }
+    int h = 0;
+    UMAP_CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    *out = h != 0;
+    return UMAP_OK;
+}
+
+bool is_device_ptr(const void* p)
+{
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+umap_status require_device(const void* p, const char* name)
+{
+    if (p && !is_device_ptr(p)) {
+        set_last_error(std::string(name) + " is not a device pointer");
+        return UMAP_ERR_NOT_DEVICE_POINTER;
+    }
+    return UMAP_OK;
+}
+
+umap_status require_cuda()
+{
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        set_last_error("no CUDA device: this library has no CPU fallback");
+        return UMAP_ERR_CUDA;
+    }
+    return UMAP_OK;
+}
+
+// a host-or-device input array made available on the device
+struct DevIn {
+    const float* p = nullptr;
+    Scratch buf;
+    umap_status make(const float* src, size_t count, cudaStream_t s)
+    {
+        if (is_device_ptr(src)) { p = src; return UMAP_OK; }
+        UMAP_TRY(buf.alloc(count * sizeof(float), s));
+        UMAP_CUDA_TRY(cudaMemcpyAsync(buf.p, src, count * sizeof(float), cudaMemcpyHostToDevice, s));
+        p = buf.as<float>();
+        return UMAP_OK;
+    }
+};
+
+struct DevOut {
+    float* p = nullptr;
+    float* host = nullptr;
+    size_t count = 0;
+    Scratch buf;
+    umap_status make(float* dst, size_t n, cudaStream_t s)
+    {
+        count = n;
+        if (is_device_ptr(dst)) { p = dst; return UMAP_OK; }
+        host = dst;
+        UMAP_TRY(buf.alloc(n * sizeof(float), s));
+        p = buf.as<float>();
+        return UMAP_OK;
+    }
+    umap_status finish(cudaStream_t s)
+    {
+        if (host) UMAP_CUDA_TRY(cudaMemcpyAsync(host, p, count * sizeof(float), cudaMemcpyDeviceToHost, s));
+        return UMAP_OK;
+    }
+};
+
+struct Timer {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st)
+    {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+    }
+    ~Timer() { cudaEventDestroy(e0); cudaEventDestroy(e1); }
+    double lap()
+    {
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        std::swap(e0, e1);
+        return ms;
+    }
+};
+
+umap_status check_params(const umap_params* p)
+{
+    if (!p || p->struct_size != sizeof(umap_params)) {
+        set_last_error("umap_params missing or struct_size mismatch (call umap_params_default)");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    if (!dim_supported(p->n_components)) {
+        set_last_error("n_components must be one of 1,2,3,4,8,16");
+        return UMAP_ERR_UNSUPPORTED;
+    }
+    if (p->negative_sample_rate < 0 || p->n_epochs < 0 || !(p->spread > 0.f) || !(p->min_dist >= 0.f)) {
+        set_last_error("invalid n_epochs / negative_sample_rate / spread / min_dist");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    if (p->knn_mode != UMAP_KNN_EXACT_FP32 && p->knn_mode != UMAP_KNN_TENSOR_BF16) {
+        set_last_error("unknown knn_mode");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    return UMAP_OK;
+}
+
+// resolved copy: a, b fitted if absent, n_epochs defaulted
+umap_status resolve(const umap_params* in, int64_t n, umap_params* out)
+{
+    *out = *in;
+    if (!(out->a > 0.f) || !(out->b > 0.f)) UMAP_TRY(umap_fit_ab(out->min_dist, out->spread, &out->a, &out->b));
+    if (out->n_epochs == 0) out->n_epochs = n <= 10000 ? 500 : 200;
+    if (out->knn_candidates < out->n_neighbors) out->knn_candidates = std::max(out->n_neighbors, 32);
+    return UMAP_OK;
+}
+
+umap_status run_knn(const umap_params* p, const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k,
+                    int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
+                    float* dist, cudaStream_t s)
+{
+    if (p->knn_mode == UMAP_KNN_TENSOR_BF16)
+        return knn_tensor(Xq, nq, Xr, nr, d, k, std::min(64, std::max(k, p->knn_candidates)), self_shift,
+                          exclude_self, index_offset, out_squared, idx, dist, s);
+    return knn_exact(Xq, nq, Xr, nr, d, k, self_shift, exclude_self, index_offset, out_squared, idx, dist, s);
+}
+
+}  // namespace
+}  // namespace umapb200
+
+using namespace umapb200;
+
+extern "C" {
+
+const char* umap_version(void) { return "umap-b200 0.1 (sm_100a)"; }
+
+int64_t umap_kernel_launch_count(void) { return g_launches; }
+
+const char* umap_last_error(void) { return g_last_error.c_str(); }
+
+const char* umap_status_string(umap_status s)
+{
+    switch (s) {
+        case UMAP_OK: return "UMAP_OK";
+        case UMAP_ERR_INVALID_ARGUMENT: return "UMAP_ERR_INVALID_ARGUMENT";
+        case UMAP_ERR_NOT_DEVICE_POINTER: return "UMAP_ERR_NOT_DEVICE_POINTER";
+        case UMAP_ERR_TOO_FEW_ROWS: return "UMAP_ERR_TOO_FEW_ROWS";
+        case UMAP_ERR_K_OUT_OF_RANGE: return "UMAP_ERR_K_OUT_OF_RANGE";
+        case UMAP_ERR_NONFINITE_INPUT: return "UMAP_ERR_NONFINITE_INPUT";
+        case UMAP_ERR_NONFINITE_EMBEDDING: return "UMAP_ERR_NONFINITE_EMBEDDING";
+        case UMAP_ERR_FIT_AB_NO_CONVERGENCE: return "UMAP_ERR_FIT_AB_NO_CONVERGENCE";
+        case UMAP_ERR_CUDA: return "UMAP_ERR_CUDA";
+        case UMAP_ERR_OUT_OF_MEMORY: return "UMAP_ERR_OUT_OF_MEMORY";
+        case UMAP_ERR_UNSUPPORTED: return "UMAP_ERR_UNSUPPORTED";
+    }
+    return "UMAP_ERR_UNKNOWN";
+}
+
+void umap_params_default(umap_params* p)
+{
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    p->struct_size = sizeof(umap_params);
+    p->n_neighbors = 15;
+    p->n_components = 2;
+    p->n_epochs = 0;
+    p->min_dist = 0.1f;
+    p->spread = 1.0f;
+    p->negative_sample_rate = 5;
+    p->learning_rate = 1.0f;
+    p->repulsion_strength = 1.0f;
+    p->a = 0.f;
+    p->b = 0.f;
+    p->seed = 0;
+    p->sgd_mode = UMAP_SGD_DETERMINISTIC;
+    p->knn_mode = UMAP_KNN_EXACT_FP32;
+    p->knn_candidates = 32;
+    p->transform_epochs = 0;
+}
+
+// R8: Levenberg-Marquardt least squares of Phi(x) = 1/(1 + a x^{2b}) against the
+// min_dist curve on linspace(0, 3 spread, 300), from (a, b) = (1, 1).
+umap_status umap_fit_ab(float min_dist, float spread, float* a_out, float* b_out)
+{
+    if (!(spread > 0.f) || !(min_dist >= 0.f) || !a_out || !b_out) {
+        set_last_error("fit_ab: spread > 0 and min_dist >= 0 required");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    const int N = 300;
+    std::vector<double> x(N), y(N);
+    for (int i = 0; i < N; ++i) {
+        x[i] = 3.0 * spread * (double)i / (double)(N - 1);
+        y[i] = x[i] < min_dist ? 1.0 : std::exp(-(x[i] - min_dist) / spread);
+    }
+    auto cost = [&](double a, double b) {
+        double c = 0;
+        for (int i = 0; i < N; ++i) {
+            const double xb = x[i] > 0 ? std::pow(x[i], 2 * b) : 0.0;
+            const double r = 1.0 / (1.0 + a * xb) - y[i];
+            c += r * r;
+        }
+        return c;
+    };
+    double a = 1.0, b = 1.0, lam = 1e-3;
+    double c = cost(a, b);
+    bool converged = false;
+    for (int it = 0; it < 2000; ++it) {
+        double jtj00 = 0, jtj01 = 0, jtj11 = 0, g0 = 0, g1 = 0;
+        for (int i = 0; i < N; ++i) {
+            if (x[i] <= 0) continue;
+            const double xb = std::pow(x[i], 2 * b);
+            const double den = 1.0 + a * xb;
+            const double f = 1.0 / den;
+            const double r = f - y[i];
+            const double da = -xb / (den * den);
+            const double db = -a * xb * 2.0 * std::log(x[i]) / (den * den);
+            jtj00 += da * da; jtj01 += da * db; jtj11 += db * db;
+            g0 += da * r; g1 += db * r;
+        }
+        bool accepted = false;
+        for (int tries = 0; tries < 60 && !accepted; ++tries) {
+            const double m00 = jtj00 * (1 + lam), m11 = jtj11 * (1 + lam), m01 = jtj01;
+            const double det = m00 * m11 - m01 * m01;
+            if (det == 0) { lam *= 10; continue; }
+            const double da = -(m11 * g0 - m01 * g1) / det;
+            const double db = -(-m01 * g0 + m00 * g1) / det;
+            const double na = a + da, nb = b + db;
+            const double nc = (nb > 0) ? cost(na, nb) : INFINITY;
+            if (nc <= c) {
+                const double rel = std::fabs(da) / std::max(1e-300, std::fabs(a)) + std::fabs(db) / std::fabs(b);
+                a = na; b = nb;
+                const double dc = c - nc;
+                c = nc;
+                lam = std::max(lam / 10, 1e-15);
+                accepted = true;
+                if (rel < 1e-14 || dc <= 1e-18 * std::max(c, 1e-300)) converged = true;
+            } else {
+                lam *= 10;
+            }
+        }
+        if (!accepted) converged = true;  // no descent direction left: at the minimum
+        if (converged) break;
+    }
+    if (!std::isfinite(a) || !std::isfinite(b) || !(a > 0) || !(b > 0)) {
+        set_last_error("fit_ab did not converge");
+        return UMAP_ERR_FIT_AB_NO_CONVERGENCE;
+    }
+    *a_out = (float)a;
+    *b_out = (float)b;
+    return UMAP_OK;
+}
+
+umap_status umap_knn(const float* X_q, int64_t n_q, const float* X_r, int64_t n_r, int32_t d, int32_t k,
+                     int64_t query_offset, int64_t index_offset, int32_t exclude_self, int32_t knn_mode,
+                     int32_t out_squared, int32_t* idx, float* dist, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_q < 0 || n_r < 1 || d < 1) { set_last_error("bad shapes"); return UMAP_ERR_INVALID_ARGUMENT; }
+    if (k < 1 || k > 64 || k > n_r - (exclude_self ? 1 : 0)) {
+        set_last_error("k out of range (1 <= k <= 64, k <= n_r - exclude_self)");
+        return UMAP_ERR_K_OUT_OF_RANGE;
+    }
+    if (n_q == 0) return UMAP_OK;
+    if (!X_q || !X_r || !idx || !dist) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
+    UMAP_TRY(require_device(X_q, "X_q"));
+    UMAP_TRY(require_device(X_r, "X_r"));
+    UMAP_TRY(require_device(idx, "idx"));
+    UMAP_TRY(require_device(dist, "dist"));
+    umap_params p;
+    umap_params_default(&p);
+    p.knn_mode = knn_mode;
+    p.n_neighbors = k;
+    UMAP_TRY(run_knn(&p, X_q, n_q, X_r, n_r, d, k, query_offset - index_offset, exclude_self != 0, index_offset,
+                     out_squared, idx, dist, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_topk_merge(const int32_t* idx_in, const float* d2_in, int32_t n_parts, int64_t n, int32_t k_in,
+                            int32_t k_out, int32_t out_squared, int32_t* idx, float* dist, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(require_device(idx_in, "idx_in"));
+    UMAP_TRY(require_device(d2_in, "d2_in"));
+    UMAP_TRY(require_device(idx, "idx"));
+    UMAP_TRY(require_device(dist, "dist"));
+    if (k_out > k_in * n_parts) { set_last_error("k_out > n_parts * k_in"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    UMAP_TRY(topk_merge(idx_in, d2_in, n_parts, n, k_in, k_out, out_squared, idx, dist, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_smooth_knn(const float* dist, const int32_t* idx, int64_t n, int32_t k, float* rho, float* sigma,
+                            float* w, int32_t* col_sorted_idx, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (k < 1 || k > 64) { set_last_error("1 <= k <= 64"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    if (!dist || !w || (col_sorted_idx && !idx)) { set_last_error("dist, w (and idx) required"); return UMAP_ERR_INVALID_ARGUMENT; }
+    UMAP_TRY(require_device(dist, "dist"));
+    UMAP_TRY(require_device(idx, "idx"));
+    UMAP_TRY(require_device(rho, "rho"));
+    UMAP_TRY(require_device(sigma, "sigma"));
+    UMAP_TRY(require_device(w, "w"));
+    UMAP_TRY(require_device(col_sorted_idx, "col_sorted_idx"));
+    UMAP_TRY(smooth_knn(dist, idx, n, k, rho, sigma, w, col_sorted_idx, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_fuzzy_union(const int32_t* idx, const float* w, int64_t n, int32_t k, int64_t* indptr, int32_t* col,
+                             float* val, int64_t capacity, int64_t* nnz, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || k < 1) { set_last_error("n >= 1, k >= 1"); return UMAP_ERR_INVALID_ARGUMENT; }
+    UMAP_TRY(require_device(idx, "idx"));
+    UMAP_TRY(require_device(w, "w"));
+    UMAP_TRY(require_device(indptr, "indptr"));
+    UMAP_TRY(require_device(col, "col"));
+    UMAP_TRY(require_device(val, "val"));
+    UMAP_TRY(fuzzy_union(idx, w, n, k, indptr, col, val, capacity, nnz, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_random_init(int64_t n, int32_t dim, uint64_t seed, float* Y, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(require_device(Y, "Y"));
+    if (dim < 1) { set_last_error("dim >= 1"); return UMAP_ERR_INVALID_ARGUMENT; }
+    UMAP_TRY(random_init(n, dim, seed, Y, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_optimize(const int64_t* indptr, const int32_t* col, const float* val, int64_t n, float* Y,
+                          const umap_params* p, int32_t e_begin, int32_t e_end, int64_t* positives, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(check_params(p));
+    if (!(p->a > 0.f) || !(p->b > 0.f) || p->n_epochs < 1) {
+        set_last_error("umap_optimize needs a > 0, b > 0, n_epochs >= 1");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    UMAP_TRY(require_device(indptr, "indptr"));
+    UMAP_TRY(require_device(col, "col"));
+    UMAP_TRY(require_device(val, "val"));
+    UMAP_TRY(require_device(Y, "Y"));
+    int64_t nnz = 0;
+    UMAP_CUDA_TRY(cudaMemcpyAsync(&nnz, indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    UMAP_TRY(optimize_layout(indptr, col, val, n, nnz, Y, p, e_begin, e_end, positives, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_transform_optimize(const int32_t* idx, const float* w, int64_t n_q, int32_t k, const float* Y_train,
+                                    int64_t n_train, float* Y_q, const umap_params* p, int32_t n_epochs_t,
+                                    int32_t e_begin, int32_t e_end, int64_t q_offset, int32_t init, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(check_params(p));
+    if (!(p->a > 0.f) || !(p->b > 0.f) || k < 1 || k > 64) {
+        set_last_error("needs a > 0, b > 0, 1 <= k <= 64");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    UMAP_TRY(require_device(idx, "idx"));
+    UMAP_TRY(require_device(w, "w"));
+    UMAP_TRY(require_device(Y_train, "Y_train"));
+    UMAP_TRY(require_device(Y_q, "Y_q"));
+    UMAP_TRY(transform_optimize(idx, w, n_q, k, Y_train, n_train, Y_q, p, n_epochs_t, e_begin, e_end, q_offset, init, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
+                               int64_t row_begin, int64_t row_end, int64_t* row_pen, int64_t* penalty, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (k < 1 || k > 64 || row_begin < 0 || row_end > n || row_begin > row_end) {
+        set_last_error("bad k or row range");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    UMAP_TRY(require_device(X, "X"));
+    UMAP_TRY(require_device(emb_idx, "emb_idx"));
+    UMAP_TRY(require_device(row_pen, "row_pen"));
+    UMAP_TRY(trust_penalty(X, n, d, emb_idx, k, row_begin, row_end, row_pen, penalty, s));
+    return UMAP_OK;
+}
+
+}  // extern "C"
+
+namespace umapb200 {
+namespace {
+
+// a3..a8 from a kNN graph already on the device (idx int32, dist fp32, n x k, rows sorted).
+umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const umap_params& p, float* Yd,
+                         umap_fit_stats& st, Timer& tm, cudaStream_t s)
+{
+    const int k = p.n_neighbors, dim = p.n_components;
+    // a3 + a4
+    Scratch acol, aw;
+    UMAP_TRY(acol.alloc(sizeof(int32_t) * (size_t)n * k, s));
+    UMAP_TRY(aw.alloc(sizeof(float) * (size_t)n * k, s));
+    UMAP_TRY(smooth_knn(dist, idx, n, k, nullptr, nullptr, aw.as<float>(), acol.as<int32_t>(), s));
+    st.ms_smooth = tm.lap();
+    // a5
+    const int64_t cap = 2 * n * (int64_t)k;
+    Scratch indptr, col, val;
+    UMAP_TRY(indptr.alloc(sizeof(int64_t) * (size_t)(n + 1), s));
+    UMAP_TRY(col.alloc(sizeof(int32_t) * (size_t)cap, s));
+    UMAP_TRY(val.alloc(sizeof(float) * (size_t)cap, s));
+    int64_t nnz = 0;
+    UMAP_TRY(fuzzy_union(acol.as<int32_t>(), aw.as<float>(), n, k, indptr.as<int64_t>(), col.as<int32_t>(),
+                         val.as<float>(), cap, &nnz, s));
+    st.ms_union = tm.lap();
+    // a7
+    UMAP_TRY(random_init(n, dim, p.seed, Yd, s));
+    st.ms_init = tm.lap();
+    // a6 + a8
+    int64_t positives = 0;
+    UMAP_TRY(optimize_layout(indptr.as<int64_t>(), col.as<int32_t>(), val.as<float>(), n, nnz, Yd, &p, 1,
+                             p.n_epochs, &positives, s));
+    st.ms_sgd = tm.lap();
+    bool bad = false;
+    UMAP_TRY(any_nonfinite(Yd, n * (int64_t)dim, &bad, s));
+    if (bad) { set_last_error("embedding became non-finite"); return UMAP_ERR_NONFINITE_EMBEDDING; }
+    st.nnz = nnz;
+    st.positives = positives;
+    st.w_max = 1.0f;
+    st.a = p.a;
+    st.b = p.b;
+    st.n_epochs = p.n_epochs;
+    return UMAP_OK;
+}
+
+}  // namespace
+}  // namespace umapb200
+
+extern "C" {
+
+umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_params* p_in, float* Y, umap_fit_stats* stats,
+                     void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(check_params(p_in));
+    const int64_t launches0 = g_launches;
+    umap_params p;
+    UMAP_TRY(resolve(p_in, n, &p));
+    const int k = p.n_neighbors, dim = p.n_components;
+    if (!X || !Y || d < 1) { set_last_error("X, Y required, d >= 1"); return UMAP_ERR_INVALID_ARGUMENT; }
+    if (k < 2 || k > 64) { set_last_error("2 <= n_neighbors <= 64"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    if (n <= k) { set_last_error("n must exceed n_neighbors"); return UMAP_ERR_TOO_FEW_ROWS; }
+
+    Timer tm(s);
+    DevIn Xd;
+    UMAP_TRY(Xd.make(X, (size_t)n * d, s));
+    DevOut Yd;
+    UMAP_TRY(Yd.make(Y, (size_t)n * dim, s));
+    bool bad = false;
+    UMAP_TRY(any_nonfinite(Xd.p, n * (int64_t)d, &bad, s));
+    if (bad) { set_last_error("X contains NaN or Inf"); return UMAP_ERR_NONFINITE_INPUT; }
+    umap_fit_stats st{};
+    double t_pre = tm.lap();
+    // a2 kNN
+    Scratch idx, dist;
+    UMAP_TRY(idx.alloc(sizeof(int32_t) * (size_t)n * k, s));
+    UMAP_TRY(dist.alloc(sizeof(float) * (size_t)n * k, s));
+    UMAP_TRY(run_knn(&p, Xd.p, n, Xd.p, n, d, k, 0, 1, 0, 0, idx.as<int32_t>(), dist.as<float>(), s));
+    st.ms_knn = tm.lap();
+    UMAP_TRY(fit_from_knn(idx.as<int32_t>(), dist.as<float>(), n, p, Yd.p, st, tm, s));
+    UMAP_TRY(Yd.finish(s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    double t_post = tm.lap();
+    st.ms_total = t_pre + st.ms_knn + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + t_post;
+    st.gpu_launches = (int32_t)(g_launches - launches0);
+    if (stats) *stats = st;
+    return UMAP_OK;
+}
+
+umap_status umap_fit_knn(const int32_t* knn_idx, const float* knn_dist, int64_t n, const umap_params* p_in, float* Y,
+                         umap_fit_stats* stats, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(check_params(p_in));
+    const int64_t launches0 = g_launches;
+    umap_params p;
+    UMAP_TRY(resolve(p_in, n, &p));
+    const int k = p.n_neighbors, dim = p.n_components;
+    if (!knn_idx || !knn_dist || !Y) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
+    if (k < 2 || k > 64) { set_last_error("2 <= n_neighbors <= 64"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    if (n <= k) { set_last_error("n must exceed n_neighbors"); return UMAP_ERR_TOO_FEW_ROWS; }
+    Timer tm(s);
+    const int32_t* idx_d = knn_idx;
+    Scratch idx_buf;
+    if (!is_device_ptr(knn_idx)) {
+        UMAP_TRY(idx_buf.alloc(sizeof(int32_t) * (size_t)n * k, s));
+        UMAP_CUDA_TRY(cudaMemcpyAsync(idx_buf.p, knn_idx, sizeof(int32_t) * (size_t)n * k, cudaMemcpyHostToDevice, s));
+        idx_d = idx_buf.as<int32_t>();
+    }
+    DevIn dist_d;
+    UMAP_TRY(dist_d.make(knn_dist, (size_t)n * k, s));
+    DevOut Yd;
+    UMAP_TRY(Yd.make(Y, (size_t)n * dim, s));
+    umap_fit_stats st{};
+    double t_pre = tm.lap();
+    UMAP_TRY(fit_from_knn(idx_d, dist_d.p, n, p, Yd.p, st, tm, s));
+    UMAP_TRY(Yd.finish(s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    double t_post = tm.lap();
+    st.ms_total = t_pre + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + t_post;
+    st.gpu_launches = (int32_t)(g_launches - launches0);
+    if (stats) *stats = st;
+    return UMAP_OK;
+}
+
+umap_status umap_transform(const float* X_train, const float* Y_train, int64_t n_train, int32_t d, const float* X_q,
+                           int64_t n_q, int64_t q_offset, const umap_params* p_in, float* Y_q, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    UMAP_TRY(check_params(p_in));
+    umap_params p;
+    UMAP_TRY(resolve(p_in, n_train, &p));
+    const int k = p.n_neighbors, dim = p.n_components;
+    if (!X_train || !Y_train || !X_q || !Y_q || d < 1) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
+    if (k < 1 || k > 64 || k > n_train) { set_last_error("1 <= k <= min(64, n_train)"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    if (n_q == 0) return UMAP_OK;
+    const int n_t = p.transform_epochs > 0 ? p.transform_epochs : (p.n_epochs + 2) / 3;
+    DevIn Xtr, Ytr, Xq;
+    UMAP_TRY(Xtr.make(X_train, (size_t)n_train * d, s));
+    UMAP_TRY(Ytr.make(Y_train, (size_t)n_train * dim, s));
+    UMAP_TRY(Xq.make(X_q, (size_t)n_q * d, s));
+    DevOut Yq;
+    UMAP_TRY(Yq.make(Y_q, (size_t)n_q * dim, s));
+    bool bad = false;
+    UMAP_TRY(any_nonfinite(Xq.p, n_q * (int64_t)d, &bad, s));
+    if (bad) { set_last_error("X_q contains NaN or Inf"); return UMAP_ERR_NONFINITE_INPUT; }
+    Scratch idx, dist, w;
+    UMAP_TRY(idx.alloc(sizeof(int32_t) * (size_t)n_q * k, s));
+    UMAP_TRY(dist.alloc(sizeof(float) * (size_t)n_q * k, s));
+    UMAP_TRY(w.alloc(sizeof(float) * (size_t)n_q * k, s));
+    UMAP_TRY(run_knn(&p, Xq.p, n_q, Xtr.p, n_train, d, k, 0, 0, 0, 0, idx.as<int32_t>(), dist.as<float>(), s));
+    UMAP_TRY(smooth_knn(dist.as<float>(), idx.as<int32_t>(), n_q, k, nullptr, nullptr, w.as<float>(), nullptr, s));
+    UMAP_TRY(transform_optimize(idx.as<int32_t>(), w.as<float>(), n_q, k, Ytr.p, n_train, Yq.p, &p, n_t, 1, n_t,
+                                q_offset, 1, s));
+    UMAP_TRY(Yq.finish(s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int32_t d_emb, int64_t n, int32_t k,
+                                 int32_t knn_mode, double* T, int64_t* penalty, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!X || !Y || !T || d < 1 || d_emb < 1) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
+    if (k < 1 || k > 64 || 2 * (int64_t)k >= n) { set_last_error("1 <= k < n/2, k <= 64"); return UMAP_ERR_K_OUT_OF_RANGE; }
+    if (knn_mode != UMAP_KNN_EXACT_FP32) { set_last_error("trust: only exact fp32 mode"); return UMAP_ERR_UNSUPPORTED; }
+    DevIn Xd, Yd;
+    UMAP_TRY(Xd.make(X, (size_t)n * d, s));
+    UMAP_TRY(Yd.make(Y, (size_t)n * d_emb, s));
+    Scratch eidx, edist;
+    UMAP_TRY(eidx.alloc(sizeof(int32_t) * (size_t)n * k, s));
+    UMAP_TRY(edist.alloc(sizeof(float) * (size_t)n * k, s));
+    UMAP_TRY(knn_exact(Yd.p, n, Yd.p, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
+    int64_t S = 0;
+    UMAP_TRY(trust_penalty(Xd.p, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, s));
+    const double nn = (double)n, kk = (double)k;
+    *T = 1.0 - (2.0 / (nn * kk * (2.0 * nn - 3.0 * kk - 1.0))) * (double)S;
+    if (penalty) *penalty = S;
+    return UMAP_OK;
+}
+
+}  // extern "C"

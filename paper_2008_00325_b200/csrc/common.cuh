@@ -1,0 +1,107 @@
+// common.cuh -- shared device helpers of the CUDA path (never shared with oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/umap_b200.h"
+
+namespace umapb200 {
+
+// ---------------------------------------------------------------- errors
+void set_last_error(const std::string& s);
+umap_status cuda_status(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define UMAP_CUDA_TRY(expr)                                              \
+    do {                                                                 \
+        cudaError_t _e = (expr);                                         \
+        if (_e != cudaSuccess) return ::umapb200::cuda_status(_e, #expr);\
+    } while (0)
+
+#define UMAP_TRY(expr)                                                   \
+    do {                                                                 \
+        umap_status _s = (expr);                                         \
+        if (_s != UMAP_OK) return _s;                                    \
+    } while (0)
+
+#define UMAP_LAUNCH_CHECK(name)                                          \
+    do {                                                                 \
+        ::umapb200::count_launch();                                      \
+        cudaError_t _e = cudaGetLastError();                             \
+        if (_e != cudaSuccess) return ::umapb200::cuda_status(_e, name); \
+    } while (0)
+
+inline int num_sms()
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync): the RMM-pool
+// analogue of P:81.  Freed on the same stream when the owner goes out of scope.
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    ~Scratch() { if (p) cudaFreeAsync(p, s); }
+    umap_status alloc(size_t bytes, cudaStream_t st)
+    {
+        s = st;
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(&p, bytes, st);
+        if (e != cudaSuccess) { p = nullptr; return cuda_status(e, "cudaMallocAsync"); }
+        return UMAP_OK;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al. SC'11; constants of the Random123 reference.  R11.
+struct u32x4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    return {c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ uint32_t pick(const u32x4& v, int i)
+{
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// key order (d2, id) of R1
+__device__ __forceinline__ bool key_less(float da, int32_t ia, float db, int32_t ib)
+{
+    return da < db || (da == db && ia < ib);
+}
+
+template <class T> __device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace umapb200

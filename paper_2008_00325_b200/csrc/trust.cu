@@ -1,0 +1,94 @@
+// trust.cu -- trustworthiness (a10; Alg. 1, R16).
+//
+// Alg. 1 batches the n x n input-space distance matrix.  Here no distance matrix
+// and no argsort exist at all: the rank of each embedding neighbour j of row i,
+// r_i(j) = 1 + #{l != i : key(d2_X(i,l), l) < key(d2_X(i,j), j)}, is obtained by
+// counting, inside the exact distance-tile kernel (knn_exact.cu, RANK epilogue),
+// how many reference rows fall below each of the k sorted thresholds of row i.
+// Penalties are exact integers summed in int64.
+#include "common.cuh"
+
+namespace umapb200 {
+
+umap_status rank_count_exact(const float* Xq, int64_t nq, const float* X, int64_t n, int d, int k,
+                             int64_t self_offset, const float* thr_d2, const int32_t* thr_id, int32_t* cnt_out,
+                             Scratch& tmp, int* n_splits_out, cudaStream_t s);
+
+namespace {
+
+// thresholds: key (d2_X(i, j_t), j_t) for the k embedding neighbours of row i, sorted by key.
+// d2 uses the exact sequential-fmaf definition (R2), identical to the tile kernel's value.
+__global__ void thresholds_kernel(const float* __restrict__ X, int d, const int32_t* __restrict__ emb_idx,
+                                  int64_t rows, int64_t row_begin, int k, float* __restrict__ thr_d2,
+                                  int32_t* __restrict__ thr_id)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const float* xi = X + (row_begin + r) * (int64_t)d;
+    float* td = thr_d2 + r * k;
+    int32_t* ti = thr_id + r * k;
+    for (int t = 0; t < k; ++t) {
+        const int32_t j = emb_idx[r * k + t];
+        const float* xj = X + (int64_t)j * d;
+        float s = 0.0f;
+        for (int f = 0; f < d; ++f) {
+            const float u = __fsub_rn(__ldg(xi + f), __ldg(xj + f));
+            s = __fmaf_rn(u, u, s);
+        }
+        int p = t;  // insertion by key
+        while (p > 0 && key_less(s, j, td[p - 1], ti[p - 1])) { td[p] = td[p - 1]; ti[p] = ti[p - 1]; --p; }
+        td[p] = s;
+        ti[p] = j;
+    }
+}
+
+// penalty of row r: counts (summed over reference splits) -> cumulative -> ranks.
+__global__ void penalty_kernel(const int32_t* __restrict__ cnt, int n_splits, int64_t rows, int k,
+                               int64_t* __restrict__ row_pen, unsigned long long* __restrict__ total)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    long long pen = 0;
+    if (r < rows) {
+        long long cum = 0;
+        for (int t = 0; t < k; ++t) {
+            for (int sp = 0; sp < n_splits; ++sp) cum += cnt[((int64_t)sp * rows + r) * k + t];
+            const long long rank = 1 + cum;
+            if (rank > k) pen += rank - k;
+        }
+        if (row_pen) row_pen[r] = pen;
+    }
+    pen = warp_sum(pen);
+    if ((threadIdx.x & 31) == 0 && pen) atomicAdd(total, (unsigned long long)pen);
+}
+
+}  // namespace
+
+umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, cudaStream_t s)
+{
+    const int64_t rows = row_end - row_begin;
+    if (rows <= 0) { if (penalty_host) *penalty_host = 0; return UMAP_OK; }
+    Scratch thr_d, thr_i, cnt, tmp, total;
+    UMAP_TRY(thr_d.alloc(sizeof(float) * (size_t)rows * k, s));
+    UMAP_TRY(thr_i.alloc(sizeof(int32_t) * (size_t)rows * k, s));
+    UMAP_TRY(cnt.alloc(sizeof(int32_t) * (size_t)rows * k, s));
+    UMAP_TRY(total.alloc(sizeof(unsigned long long), s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(total.p, 0, sizeof(unsigned long long), s));
+    thresholds_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(),
+                                                          thr_i.as<int32_t>());
+    UMAP_LAUNCH_CHECK("thresholds_kernel");
+    int n_splits = 1;
+    UMAP_TRY(rank_count_exact(X + row_begin * (int64_t)d, rows, X, n, d, k, row_begin, thr_d.as<float>(),
+                              thr_i.as<int32_t>(), cnt.as<int32_t>(), tmp, &n_splits, s));
+    const int32_t* counts = n_splits == 1 ? cnt.as<int32_t>() : tmp.as<int32_t>();
+    penalty_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(counts, n_splits, rows, k, row_pen,
+                                                       total.as<unsigned long long>());
+    UMAP_LAUNCH_CHECK("penalty_kernel");
+    unsigned long long S = 0;
+    UMAP_CUDA_TRY(cudaMemcpyAsync(&S, total.p, sizeof(S), cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    if (penalty_host) *penalty_host = (int64_t)S;
+    return UMAP_OK;
+}
+
+}  // namespace umapb200

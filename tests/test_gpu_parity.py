@@ -1,0 +1,350 @@
+"""GPU-vs-oracle parity through the C ABI (task rule ③).  Run on a B200: pytest -m gpu.
+
+Tolerances (BASELINE.json north_star):
+  kNN exact mode ............ indices and distances bit-exact
+  rho ........................ bit-exact;  sigma <= 1 fp32 ulp
+  fuzzy weights .............. <= 1e-5 relative, CSR structure identical
+  deterministic SGD .......... <= 1e-4 absolute per epoch (teacher-forced)
+  Hogwild / end-to-end ....... trustworthiness within 0.005 of the oracle
+  trustworthiness (exact) .... integer penalty identical
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # the marker deselects these on CPU runs; be explicit anyway
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2008_00325_b200 as U  # noqa: E402
+
+A_, B_ = 1.5769434603, 0.8950608779
+DEV = "cuda"
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def ulp_diff(a, b):
+    a = np.asarray(a, np.float32).view(np.int32).astype(np.int64)
+    b = np.asarray(b, np.float32).view(np.int32).astype(np.int64)
+    return np.abs(a - b)
+
+
+# ------------------------------------------------------------------- kNN (a2)
+KNN_CASES = [
+    # (n, d, k, data)  -- several 128-row tiles, ragged row tails and ragged 16-feature K tails
+    (1000, 50, 15, "lowrank"),
+    (700, 784, 15, "lowrank"),
+    (517, 64, 1, "lowrank"),
+    (900, 33, 33, "iso"),
+    (400, 8, 64, "lowrank"),
+    (600, 3, 15, "ties"),
+    (129, 17, 15, "ties"),
+    (20, 5, 19, "lowrank"),
+]
+
+
+def _data(kind, n, d, seed=0):
+    if kind == "lowrank":
+        return synth.lowrank(n, d, blobs=5, seed=seed)
+    if kind == "iso":
+        return synth.iso(n, d, blobs=5, seed=seed)
+    return synth.ties(n, d, seed=seed)
+
+
+@pytest.mark.parametrize("n,d,k,kind", KNN_CASES)
+def test_knn_exact_bitexact(O, n, d, k, kind):
+    X = _data(kind, n, d)
+    ri, rd = O.knn(X, X, k, self_offset=0)
+    gi, gd = U.knn(cu(X), cu(X), k, exclude_self=True)
+    assert np.array_equal(np_(gi), ri)
+    assert np.array_equal(np_(gd).view(np.int32), rd.view(np.int32))
+
+
+def test_knn_exact_query_vs_reference_offsets(O):
+    X = synth.lowrank(1500, 40, seed=1)
+    Xq, Xr = X[:230], X[230:]
+    ri, rd = O.knn(Xq, Xr, 12, self_offset=-1)
+    gi, gd = U.knn(cu(Xq), cu(Xr), 12, index_offset=1000)
+    assert np.array_equal(np_(gi), ri + 1000)
+    assert np.array_equal(np_(gd), rd)
+    gi2, gd2 = U.knn(cu(Xq), cu(Xr), 12, squared=True)
+    assert np.array_equal(np.sqrt(np_(gd2)), rd)
+
+
+def test_knn_split_reference_and_topk_merge(O):
+    # few queries vs many references exercises the split-R path (merge kernel)
+    X = synth.lowrank(6000, 24, seed=2)
+    Xq = X[:40]
+    ri, rd = O.knn(Xq, X, 15, self_offset=0)
+    gi, gd = U.knn(cu(Xq), cu(X), 15, exclude_self=True)
+    assert np.array_equal(np_(gi), ri) and np.array_equal(np_(gd), rd)
+    # explicit shard merge: 3 reference shards with global ids, squared distances
+    parts_i, parts_d = [], []
+    bounds = [0, 1700, 4100, 6000]
+    for s in range(3):
+        lo, hi = bounds[s], bounds[s + 1]
+        pi, pd = U.knn(cu(Xq), cu(X[lo:hi]), 15, exclude_self=True, query_offset=0, index_offset=lo,
+                       squared=True)
+        parts_i.append(pi)
+        parts_d.append(pd)
+    mi, md = U.topk_merge(torch.stack(parts_i), torch.stack(parts_d), 15)
+    assert np.array_equal(np_(mi), ri) and np.array_equal(np_(md), rd)
+
+
+def test_knn_empty_query_and_errors():
+    X = cu(synth.lowrank(50, 4))
+    gi, gd = U.knn(X[:0], X, 5)
+    assert gi.shape == (0, 5)
+    with pytest.raises(RuntimeError):
+        U.knn(X, X, 50, exclude_self=True)  # k > n - 1
+
+
+# ------------------------------------------------------------------- rho/sigma/w (a3, a4)
+@pytest.mark.parametrize("n,d,k", [(1000, 30, 15), (333, 10, 5), (500, 64, 50), (260, 4, 2)])
+def test_smooth_knn_parity(O, n, d, k):
+    X = synth.lowrank(n, d, seed=3)
+    idx, dist = O.knn(X, X, k, self_offset=0)
+    rho, sigma = O.smooth_knn(dist)
+    w = O.membership(dist, rho, sigma)
+    g_rho, g_sigma, g_w, g_cs = U.smooth_knn(cu(dist), cu(idx), sort_by_col=True)
+    assert np.array_equal(np_(g_rho), rho)
+    assert ulp_diff(np_(g_sigma), sigma).max() <= 1
+    # column-sorted rows: same (col, w) pairs re-ordered
+    order = np.argsort(idx, axis=1, kind="stable")
+    assert np.array_equal(np_(g_cs), np.take_along_axis(idx, order, 1))
+    gw = np_(g_w)
+    ref = np.take_along_axis(w, order, 1)
+    assert np.all(np.abs(gw - ref) <= 1e-5 * np.abs(ref))
+    _, _, g_w2 = U.smooth_knn(cu(dist))
+    assert np.all(np.abs(np_(g_w2) - w) <= 1e-5 * np.abs(w))
+
+
+def test_smooth_knn_degenerate_rows(O):
+    dist = np.array([[0, 0, 0, 0], [2.5, 2.5, 2.5, 2.5], [0, 1, 2, 3], [1, 2, 2, 2]], np.float32)
+    idx = np.array([[1, 2, 3, 0], [0, 2, 3, 1], [0, 1, 3, 2], [0, 1, 2, 3]], np.int32)
+    rho, sigma = O.smooth_knn(dist)
+    g_rho, g_sigma, g_w = U.smooth_knn(cu(dist), cu(idx))
+    assert np.array_equal(np_(g_rho), rho) and ulp_diff(np_(g_sigma), sigma).max() <= 1
+    assert np.allclose(np_(g_w), O.membership(dist, rho, sigma), rtol=1e-5)
+
+
+# ------------------------------------------------------------------- union (a5)
+@pytest.mark.parametrize("n,d,k,kind", [(1200, 20, 15, "lowrank"), (900, 64, 15, "iso"), (300, 3, 10, "ties")])
+def test_fuzzy_union_parity(O, n, d, k, kind):
+    X = _data(kind, n, d, seed=4)
+    idx, dist = O.knn(X, X, k, self_offset=0)
+    rho, sigma = O.smooth_knn(dist)
+    w = O.membership(dist, rho, sigma)
+    r_indptr, r_col, r_val = O.fuzzy_union(idx, w)
+    order = np.argsort(idx, axis=1, kind="stable")
+    cs = np.take_along_axis(idx, order, 1)
+    ws = np.take_along_axis(w, order, 1)
+    g_indptr, g_col, g_val = U.fuzzy_union(cu(cs), cu(ws))
+    assert np.array_equal(np_(g_indptr), r_indptr)
+    assert np.array_equal(np_(g_col), r_col)
+    assert np.all(np.abs(np_(g_val) - r_val) <= 1e-5 * r_val)
+
+
+def test_fuzzy_union_hub_rows(O):
+    # a hub: row 0 at the origin, the others at radius ~1 in random directions of a
+    # 50-D space (nearly orthogonal, mutual distance ~1.4): row 0 is everybody's
+    # nearest neighbour, so A^T row 0 is far longer than a warp
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((400, 50)).astype(np.float32)
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    X *= rng.uniform(1, 1.1, (400, 1)).astype(np.float32)
+    X[0] = 0
+    idx, dist = O.knn(X, X, 8, self_offset=0)
+    assert (idx == 0).sum() > 64
+    rho, sigma = O.smooth_knn(dist)
+    w = O.membership(dist, rho, sigma)
+    r = O.fuzzy_union(idx, w)
+    order = np.argsort(idx, axis=1, kind="stable")
+    g = U.fuzzy_union(cu(np.take_along_axis(idx, order, 1)), cu(np.take_along_axis(w, order, 1)))
+    assert np.array_equal(np_(g[0]), r[0]) and np.array_equal(np_(g[1]), r[1])
+    assert np.all(np.abs(np_(g[2]) - r[2]) <= 1e-5 * r[2])
+
+
+# ------------------------------------------------------------------- init (a7)
+def test_random_init_bitexact(O):
+    for dim, seed in [(2, 0), (3, 12345678901234), (16, 7)]:
+        assert np.array_equal(np_(U.random_init(3001, dim, seed)), O.random_init(3001, dim, seed))
+
+
+# ------------------------------------------------------------------- SGD (a6, a8)
+def _graph(O, n=1500, d=32, k=15, seed=5, kind="lowrank"):
+    X = _data(kind, n, d, seed=seed)
+    _, _, _, _, _, (indptr, col, val) = O.fuzzy_graph(X, k)
+    return X, indptr, col, val
+
+
+@pytest.mark.parametrize("kind", ["lowrank", "iso"])
+def test_sgd_deterministic_teacher_forced(O, kind):
+    X, indptr, col, val = _graph(O, kind=kind)
+    n = X.shape[0]
+    N = 200
+    Y = synth.uniform_embedding(n, 2, seed=1)
+    for e in (1, 2, 57, 120, 199):
+        ref = O.optimize(indptr, col, val, Y, A_, B_, N, e_begin=e, e_end=e + 1, m=5, seed=11)
+        Yg = cu(Y)
+        U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=e, e_end=e + 1, n_epochs=N, a=A_, b=B_, seed=11,
+                   sgd_mode="deterministic")
+        err = np.abs(np_(Yg) - ref).max()
+        assert err <= 1e-4, (e, err)
+        Y = ref  # teacher forcing: next epoch starts from the oracle's state
+
+
+def test_sgd_deterministic_reproducible_and_dims(O):
+    X, indptr, col, val = _graph(O, n=900)
+    for dim in (2, 3, 16):
+        Y0 = cu(synth.uniform_embedding(900, dim, seed=2))
+        outs = []
+        for _ in range(2):
+            Yg = Y0.clone()
+            U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=1, e_end=30, n_epochs=30, a=A_, b=B_, seed=3)
+            outs.append(np_(Yg))
+        assert np.array_equal(outs[0], outs[1])
+        ref = O.optimize(indptr, col, val, np_(Y0), A_, B_, 30, e_begin=5, e_end=6, m=5, seed=3)
+        Yg = Y0.clone()
+        U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=5, e_end=6, n_epochs=30, a=A_, b=B_, seed=3)
+        assert np.abs(np_(Yg) - ref).max() <= 1e-4
+
+
+def test_sgd_positive_count_matches_schedule(O):
+    X, indptr, col, val = _graph(O, n=600)
+    N = 50
+    r = (val / val.max()).astype(np.float32)
+    expected = sum(int(np.sum(np.floor(np.float32(e) * r) > np.floor(np.float32(e - 1) * r))) for e in range(1, N))
+    Yg = cu(synth.uniform_embedding(600, 2))
+    pos = U.optimize(cu(indptr), cu(col), cu(val), Yg, n_epochs=N, a=A_, b=B_)
+    assert pos == expected
+
+
+# ------------------------------------------------------------------- end to end
+def test_fit_c1_digits_vs_oracle(O):
+    X = synth.make("C1")
+    ref = O.fit(X, k=15, n_epochs=200, a=A_, b=B_, seed=0, mode="deterministic")
+    t_ref = O.trustworthiness(X, ref, 15)
+    for mode in ("deterministic", "hogwild"):
+        Y, st = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=0, sgd_mode=mode)
+        T, _ = U.trustworthiness(cu(X), Y, 15)
+        assert abs(T - t_ref) <= 0.005, (mode, T, t_ref)
+        assert st["gpu_launches"] > 200 and st["nnz"] > 0
+
+
+def test_fit_host_pointers_equal_device(O):
+    X = synth.lowrank(800, 16, seed=6)
+    Yd, _ = U.fit(cu(X), n_epochs=60, a=A_, b=B_, seed=4)
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh, _ = U.fit(Xh, n_epochs=60, a=A_, b=B_, seed=4)
+    assert not Yh.is_cuda
+    assert np.array_equal(np_(Yd), Yh.numpy())
+
+
+def test_fit_rejects_nonfinite_and_tiny():
+    X = synth.lowrank(100, 4)
+    X[3, 2] = np.nan
+    with pytest.raises(RuntimeError, match="NONFINITE"):
+        U.fit(cu(X), n_epochs=10)
+    with pytest.raises(RuntimeError, match="TOO_FEW_ROWS"):
+        U.fit(cu(synth.lowrank(15, 4)), n_neighbors=15)
+
+
+def test_fit_minimum_rows():
+    Y, _ = U.fit(cu(synth.lowrank(16, 3)), n_neighbors=15, n_epochs=20)
+    assert torch.isfinite(Y).all()
+
+
+# ------------------------------------------------------------------- transform (a9)
+def _transform_setup(O, n_tr=1200, n_q=700, d=24, k=15):
+    X = synth.lowrank(n_tr + n_q, d, seed=7)
+    Xtr, Xq = X[:n_tr], X[n_tr:]
+    Ytr = O.fit(Xtr, k=k, n_epochs=40, a=A_, b=B_, seed=1)
+    idx, dist = O.knn(Xq, Xtr, k)
+    rho, sigma = O.smooth_knn(dist)
+    w = O.membership(dist, rho, sigma)
+    return Xtr, Xq, Ytr, idx, dist, w
+
+
+def test_transform_init_and_teacher_forced(O):
+    Xtr, Xq, Ytr, idx, dist, w = _transform_setup(O)
+    Nt = 67
+    y0 = O.transform_init(idx, w, Ytr)
+    Yg = torch.zeros((Xq.shape[0], 2), dtype=torch.float32, device=DEV)
+    U.transform_optimize(cu(idx), cu(w), cu(Ytr), Yg, Nt, e_begin=1, e_end=1, init=True, a=A_, b=B_)
+    assert np.array_equal(np_(Yg), y0)
+    # per-epoch teacher forcing.  Each query row chains k (1 + m) = 90 dependent in-place
+    # updates per epoch, so fp32-vs-fp64 rounding is amplified along the chain
+    # (DESIGN.md "Parity bars"): bar = 99.9 % of rows within 1e-4, every row within 1e-3.
+    Y = y0
+    errs = []
+    for e in range(1, Nt):
+        ref = O.transform_optimize(idx, w, Ytr, Y, A_, B_, Nt, seed=9, e_begin=e, e_end=e + 1)
+        Yg = cu(Y)
+        U.transform_optimize(cu(idx), cu(w), cu(Ytr), Yg, Nt, e_begin=e, e_end=e + 1, a=A_, b=B_, seed=9)
+        errs.append(np.abs(np_(Yg) - ref).max(1))
+        Y = ref
+    errs = np.array(errs)
+    assert errs.max() <= 1e-3, errs.max()
+    assert np.quantile(errs, 0.999) <= 1e-4
+
+
+def test_transform_end_to_end_and_partition_invariance(O):
+    Xtr, Xq, Ytr, idx, dist, w = _transform_setup(O)
+    ref = O.transform(Xtr, Ytr, Xq, k=15, n_epochs=200, a=A_, b=B_, seed=3)
+    Ytr_before = Ytr.copy()
+    full = U.transform(cu(Xtr), cu(Ytr), cu(Xq), n_epochs=200, a=A_, b=B_, seed=3)
+    assert np.array_equal(Ytr, Ytr_before)
+    # contractive towards the frozen anchors: end-to-end drift stays small
+    assert np.abs(np_(full) - ref).max() < 1e-2
+    parts = [U.transform(cu(Xtr), cu(Ytr), cu(Xq[a:b]), q_offset=a, n_epochs=200, a=A_, b=B_, seed=3)
+             for a, b in [(0, 123), (123, 500), (500, 700)]]
+    assert np.array_equal(np_(torch.cat(parts)), np_(full))
+
+
+# ------------------------------------------------------------------- trust (a10)
+@pytest.mark.parametrize("n,d,k", [(700, 20, 15), (1000, 64, 5), (300, 7, 1), (257, 3, 40)])
+def test_trust_penalty_exact(O, n, d, k):
+    X = synth.lowrank(n, d, seed=8)
+    Y = synth.uniform_embedding(n, 2, seed=9)
+    S_ref, pen_ref = O.trust_penalty(X, Y, k)
+    T, S = U.trustworthiness(cu(X), cu(Y), k)
+    assert S == S_ref
+    assert T == O.trust_from_penalty(S_ref, n, k)
+    emb_idx, _ = O.knn(Y, Y, k, self_offset=0)
+    S2, pen = U.trust_penalty(cu(X), cu(emb_idx[100:250]), k, 100, 250)
+    assert np.array_equal(np_(pen), pen_ref[100:250])
+
+
+def test_trust_identity_is_one():
+    X = cu(synth.lowrank(500, 6))
+    T, S = U.trustworthiness(X, X, 10)
+    assert S == 0 and T == 1.0
+
+
+# ------------------------------------------------------------------- full-size sampled checks
+@pytest.mark.slow
+def test_c2_full_size_sampled_knn_and_trust(O):
+    """C2 at full size (70,000 x 784) in the launch configuration bench.py times: sampled
+    rows are recomputed one by one by the oracle."""
+    X = synth.make("C2")
+    Xg = cu(X)
+    gi, gd = U.knn(Xg, Xg, 15, exclude_self=True)
+    gi, gd = np_(gi), np_(gd)
+    rng = np.random.default_rng(0)
+    rows = np.concatenate([[0, 69999], rng.choice(70000, 10, replace=False)])
+    for r in rows:
+        ri, rd = O.knn(X[r:r + 1], X, 15, self_offset=int(r))
+        assert np.array_equal(gi[r], ri[0]) and np.array_equal(gd[r], rd[0])
