@@ -101,6 +101,21 @@ umap_status require_cuda()
         set_last_error("no CUDA device: this library has no CPU fallback");
         return UMAP_ERR_CUDA;
     }
+    // Keep freed stream-ordered scratch in the device pool instead of unmapping it at
+    // every synchronisation (the default release threshold is 0): the single
+    // per-process memory pool of P:81 / P:105.  Once per device.
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        configured_dev = dev;
+    }
     return UMAP_OK;
 }
 

@@ -1,13 +1,645 @@
-// knn_tensor.cu -- tensor-core candidate kNN (R3).  Placeholder until the tcgen05 path lands.
+// knn_tensor.cu -- tensor-core candidate kNN (R3) with exact re-rank.
+//
+// a2 in TENSOR_BF16 mode (north_star "a tcgen05/TMA tensor-core GEMM fused
+// with a register/shared-memory top-k select").
+//
+//  1. prep (a1): column means (fp64), Xc = bf16(X - mean) zero-padded to d_pad =
+//     ceil(d/64)*64, row norms ||bf16 xc||^2 in fp32.
+//  2. knn_tc_kernel: per CTA one block of 128 query rows against a range of reference
+//     rows, 256 references per tile.  Warp-specialised:
+//        warp 0  TMA producer: A (128 x 64 bf16) + B (256 x 64 bf16) K-slabs into a
+//                3-stage smem ring (SWIZZLE_128B), mbarrier full/empty handshake;
+//        warp 1  TMEM owner + MMA issuer: one thread issues tcgen05.mma.kind::f16
+//                (M=128, N=256, K=16; BF16 in, FP32 accumulate in TMEM), two 256-column
+//                accumulators so tile t+1 is multiplied while tile t is filtered;
+//        warps 2-5 epilogue: tcgen05.ld of the accumulator row owned by each thread,
+//                d2~ = |q|^2 + |r|^2 - 2 q.r, running top-k' (k' <= 64) per query row
+//                sorted in registers (one thread per row).
+//  3. rerank_kernel: warp per query, lane per candidate: exact fp32 d2 (R2 definition,
+//     sequential fmaf over features), bitonic sort of the k' keys (d2, id), top k.
+//     Whenever the candidate set holds the true k nearest the output equals the exact
+//     mode bit for bit.
+#include <cuda.h>
+#include <cstdlib>
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace umapb200 {
 
-umap_status knn_tensor(const float*, int64_t, const float*, int64_t, int, int, int, int64_t, int, int64_t, int,
-                       int32_t*, float*, cudaStream_t)
+umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
+                       int out_squared, int32_t* idx, float* dist, cudaStream_t s);
+
+namespace {
+
+constexpr int TC_BM = 128;        // query rows per CTA (TMEM lanes)
+constexpr int TC_BN = 256;        // reference rows per tile (UMMA N)
+constexpr int TC_BK = 64;         // K slab = 64 bf16 = 128 B (one SWIZZLE_128B atom row)
+constexpr int TC_KCMAX = 64;      // max candidates per query row (k')
+constexpr int TC_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half of the columns
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;   // producer + MMA + epilogue warps
+constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
+constexpr uint32_t B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+
+// ----------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
-    set_last_error("knn_mode TENSOR_BF16 not built yet");
-    return UMAP_ERR_UNSUPPORTED;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart (SBO),
+// LBO unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+    d |= (uint64_t)1 << 46;                 // version
+    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: kind::f16, A=B=BF16, D=F32, both K-major, M=128, N=256
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+                           ((uint32_t)(TC_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+    const float* qnorm;     // [n_q]
+    const float* rnorm;     // [n_r]
+    int64_t nq, nr;
+    int kblocks;            // d_pad / 64
+    int kc;                 // candidates kept per row (<= 32)
+    int64_t split_len;      // reference rows per split (multiple of TC_BN)
+    int64_t self_shift;     // local reference j is query q's own row when j == q + self_shift
+    int exclude_self;
+    int64_t index_offset;   // global id = j + index_offset
+    int debug;              // bit0: skip epilogue filtering, bit1: skip MMA issue (profiling only)
+    int32_t* cand_idx;      // [split][n_q][kc]
+    float* cand_d2;
+};
+
+template <int KC, int TC_STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_r, TcArgs a)
+{
+    extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    uint8_t* smem = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* stage_base = smem;                                     // TC_STAGES x (A | B)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);  // full[S], empty[S], tfull[2], tempty[2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q0 = (int64_t)blockIdx.x * TC_BM;
+    const int64_t r_lo = (int64_t)blockIdx.y * a.split_len;
+    const int64_t r_hi = imin64(a.nr, r_lo + a.split_len);
+    const int ntiles = (int)((r_hi - r_lo + TC_BN - 1) / TC_BN);
+    const int KB = a.kblocks;
+
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
+    const uint32_t tfull0 = smem_u32(bars + 2 * TC_STAGES), tempty0 = smem_u32(bars + 2 * TC_STAGES + 2);
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(tfull0 + 8 * b, 1);
+            mbar_init(tempty0 + 8 * b, TC_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_q) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_r) : "memory");
+    }
+    if (warp == 1) {  // TMEM: 512 columns = two 128x256 fp32 accumulators
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            int g = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                const int y_r = (int)(r_lo + (int64_t)t * TC_BN);
+                for (int kb = 0; kb < KB; ++kb, ++g) {
+                    const int s = g % TC_STAGES;
+                    const uint32_t ph = (g / TC_STAGES) & 1;
+                    mbar_wait(empty0 + 8 * s, ph ^ 1);
+                    const uint32_t dst = smem_u32(stage_base + s * STAGE_BYTES);
+                    mbar_expect_tx(full0 + 8 * s, STAGE_BYTES);
+                    tma_load_2d(dst, &map_q, kb * TC_BK, (int)q0, full0 + 8 * s);
+                    tma_load_2d(dst + A_BYTES, &map_r, kb * TC_BK, y_r, full0 + 8 * s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            int g = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                const int b = t & 1;
+                mbar_wait(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + (uint32_t)(b * TC_BN);
+                for (int kb = 0; kb < KB; ++kb, ++g) {
+                    const int s = g % TC_STAGES;
+                    const uint32_t ph = (g / TC_STAGES) & 1;
+                    mbar_wait(full0 + 8 * s, ph);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(stage_base + s * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < TC_BK / 16; ++kk) {
+                        if (!(a.debug & 2)) umma_bf16(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                                  (kb | kk) != 0);
+                    }
+                    umma_commit(empty0 + 8 * s);  // smem slot free once these MMAs have read it
+                }
+                umma_commit(tfull0 + 8 * b);      // accumulator b complete
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue (warps 2..9)
+        // Warp w reads TMEM lane quadrant w % 4 (hardware restriction) and half
+        // h = (w - 2) / 4 of each tile's 256 columns.  Each thread owns one query row and
+        // keeps its k' best approximate keys of its half sorted in registers.  Per 32
+        // columns: one tcgen05.ld, 32 independent d2 = |q|^2 + |r|^2 - 2 q.r, one warp vote;
+        // only when some lane holds a candidate below its threshold does the warp run the
+        // branch-free compare-exchange insertion for that column.  The two halves of a row
+        // are merged through shared memory at the end.
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quad * 32 + lane;
+        const int64_t q = q0 + row;
+        const bool valid = q < a.nq;
+        const float qn = valid ? a.qnorm[q] : 0.0f;
+        const int64_t self_j = (valid && a.exclude_self) ? q + a.self_shift : -1;
+        float kd[KC];
+        int32_t ki[KC];
+#pragma unroll
+        for (int i = 0; i < KC; ++i) { kd[i] = INFINITY; ki[i] = -1; }
+        float thr = INFINITY;
+        for (int t = 0; t < ntiles; ++t) {
+            const int b = t & 1;
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
+            tc_fence_after();
+            const int64_t rb = r_lo + (int64_t)t * TC_BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
+#pragma unroll 1
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
+                float v[32];
+                tmem_ld32(taddr + c, v);
+                const int64_t jb = rb + c;
+                const float rn_l = (jb + lane < r_hi) ? __ldg(a.rnorm + jb + lane) : INFINITY;
+                uint32_t cm = 0;  // columns of this chunk that beat the running threshold
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const float rn = __shfl_sync(0xffffffffu, rn_l, u);
+                    v[u] = fmaf(-2.0f, v[u], qn + rn);
+                    cm |= (uint32_t)(v[u] < thr) << u;
+                }
+                if (!valid) cm = 0;
+                if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
+                // one insertion round per candidate of the busiest lane; each lane inserts its
+                // lowest remaining candidate (selected from registers by a 5-level select tree)
+                while (__any_sync(0xffffffffu, cm != 0)) {
+                    const int u = cm ? __ffs(cm) - 1 : 0;
+                    const bool has = cm != 0;
+                    cm &= cm - 1;
+                    float w16[16], w8[8], w4[4], w2[2];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) w16[i] = (u & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w8[i] = (u & 2) ? w16[2 * i + 1] : w16[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) w4[i] = (u & 4) ? w8[2 * i + 1] : w8[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) w2[i] = (u & 8) ? w4[2 * i + 1] : w4[2 * i];
+                    const float sel = (u & 16) ? w2[1] : w2[0];
+                    float cv = (has && sel < thr) ? sel : INFINITY;
+                    int32_t ci = (int32_t)(jb + u + a.index_offset);
+#pragma unroll
+                    for (int i = 0; i < KC; ++i) {
+                        const bool sw = cv < kd[i];
+                        const float tk = sw ? kd[i] : cv;
+                        const int32_t ti = sw ? ki[i] : ci;
+                        kd[i] = sw ? cv : kd[i];
+                        ki[i] = sw ? ci : ki[i];
+                        cv = tk;
+                        ci = ti;
+                    }
+                    thr = kd[KC - 1];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+        }
+        // merge the two halves of each row: half 1 publishes its list through smem (the
+        // stage ring is idle now: every TMA load has been consumed by the last MMA)
+        float* xd = reinterpret_cast<float*>(stage_base);
+        int32_t* xi = reinterpret_cast<int32_t*>(stage_base) + KC * TC_BM;
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");  // all MMAs done reading smem
+        if (half == 1) {
+#pragma unroll
+            for (int i = 0; i < KC; ++i) { xd[i * TC_BM + row] = kd[i]; xi[i * TC_BM + row] = ki[i]; }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+        if (half == 0) {
+            for (int m = 0; m < KC; ++m) {
+                float cv = xd[m * TC_BM + row];
+                int32_t ci = xi[m * TC_BM + row];
+                if (!(cv < kd[KC - 1])) break;  // the other list is sorted: nothing better follows
+#pragma unroll
+                for (int i = 0; i < KC; ++i) {
+                    const bool sw = cv < kd[i];
+                    const float tk = sw ? kd[i] : cv;
+                    const int32_t ti = sw ? ki[i] : ci;
+                    kd[i] = sw ? cv : kd[i];
+                    ki[i] = sw ? ci : ki[i];
+                    cv = tk;
+                    ci = ti;
+                }
+            }
+            if (valid) {
+                const int kc = a.kc;
+                const int64_t base = ((int64_t)blockIdx.y * a.nq + q) * kc;
+#pragma unroll
+                for (int t = 0; t < KC; ++t) {
+                    if (t < kc) {
+                        a.cand_idx[base + t] = ki[t];
+                        a.cand_d2[base + t] = kd[t];
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+}
+
+// ----------------------------------------------------------------------------- prep
+__global__ void colsum_kernel(const float* __restrict__ X, int64_t n, int d, double* __restrict__ colsum)
+{
+    // block (32 columns x 8 row lanes); grid (ceil(d/32), row chunks)
+    __shared__ double part[8][33];
+    const int cx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int col = blockIdx.x * 32 + cx;
+    double s = 0.0;
+    if (col < d)
+        for (int64_t r = (int64_t)blockIdx.y * 8 + ry; r < n; r += (int64_t)gridDim.y * 8) s += (double)X[r * d + col];
+    part[ry][cx] = s;
+    __syncthreads();
+    if (ry == 0 && col < d) {
+        double t = 0.0;
+        for (int i = 0; i < 8; ++i) t += part[i][cx];
+        atomicAdd(colsum + col, t);
+    }
+}
+
+__global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
+                                   const double* __restrict__ colsum, double inv_n, __nv_bfloat16* __restrict__ Xc,
+                                   float* __restrict__ norms)
+{
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    float acc = 0.0f;
+    for (int f = lane; f < d_pad; f += 32) {
+        __nv_bfloat16 h = __float2bfloat16_rn(0.0f);
+        if (f < d) {
+            const float c = X[row * d + f] - (float)(colsum[f] * inv_n);
+            h = __float2bfloat16_rn(c);
+            const float hv = __bfloat162float(h);
+            acc = fmaf(hv, hv, acc);
+        }
+        Xc[row * d_pad + f] = h;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) norms[row] = acc;
+}
+
+// ----------------------------------------------------------------------------- re-rank
+// warp per query row; candidates t and t + 32 on lane t (kc <= 64); exact fp32 d2 (R2),
+// a bitonic sort of each 32-wide half by key (d2, id), then the two sorted halves are
+// merged by rank (keys are distinct: ids differ) and the first k written.
+__device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)
+{
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const float ok = __shfl_xor_sync(0xffffffffu, key, stride);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
+            const bool up = ((lane & size) == 0);
+            const bool lower = (lane & stride) == 0;
+            const bool other_less = key_less(ok, oi, key, id);
+            const bool take = lower ? (up ? other_less : !other_less) : (up ? !other_less : other_less);
+            if (take && !(ok == key && oi == id)) { key = ok; id = oi; }
+        }
+    }
+}
+
+// R2 exact distance: sequential fmaf in ascending feature order (float4 loads when the
+// rows are 16-byte aligned; the accumulation order is unchanged).
+__device__ __forceinline__ float exact_d2(const float* x, const float* y, int d)
+{
+    float s = 0.0f;
+    int f = 0;
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* y4 = reinterpret_cast<const float4*>(y);
+        for (; f + 4 <= d; f += 4) {
+            const float4 a = __ldg(x4 + (f >> 2)), b = __ldg(y4 + (f >> 2));
+            float t = __fsub_rn(a.x, b.x); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.y, b.y); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.z, b.z); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.w, b.w); s = __fmaf_rn(t, t, s);
+        }
+    }
+    for (; f < d; ++f) {
+        const float t = __fsub_rn(__ldg(x + f), __ldg(y + f));
+        s = __fmaf_rn(t, t, s);
+    }
+    return s;
+}
+
+__global__ void rerank_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
+                              const int32_t* __restrict__ cand, int kc, int64_t index_offset, int k, int out_squared,
+                              int32_t* __restrict__ idx, float* __restrict__ dist)
+{
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= nq) return;
+    const float* x = Xq + q * (int64_t)d;
+    float key[2] = {INFINITY, INFINITY};
+    int32_t id[2] = {INT32_MAX, INT32_MAX};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = lane + 32 * h;
+        const int32_t c = t < kc ? cand[q * kc + t] : -1;
+        if (c >= 0) {
+            key[h] = exact_d2(x, Xr + (int64_t)(c - index_offset) * d, d);
+            id[h] = c;
+        }
+    }
+    warp_bitonic(key[0], id[0], lane);
+    if (kc > 32) {
+        warp_bitonic(key[1], id[1], lane);
+        // position of each element in the merged order: own index + rank in the other half
+        int pos0 = lane, pos1 = lane;
+        for (int j = 0; j < 32; ++j) {  // ballot-free: compare against every element of the other half
+            const float ok1 = __shfl_sync(0xffffffffu, key[1], j);
+            const int32_t oi1 = __shfl_sync(0xffffffffu, id[1], j);
+            const float ok0 = __shfl_sync(0xffffffffu, key[0], j);
+            const int32_t oi0 = __shfl_sync(0xffffffffu, id[0], j);
+            pos0 += key_less(ok1, oi1, key[0], id[0]);
+            pos1 += key_less(ok0, oi0, key[1], id[1]);
+        }
+        if (pos0 < k) {
+            idx[q * k + pos0] = id[0] == INT32_MAX ? -1 : id[0];
+            dist[q * k + pos0] = out_squared ? key[0] : (isinf(key[0]) ? key[0] : __fsqrt_rn(key[0]));
+        }
+        if (pos1 < k) {
+            idx[q * k + pos1] = id[1] == INT32_MAX ? -1 : id[1];
+            dist[q * k + pos1] = out_squared ? key[1] : (isinf(key[1]) ? key[1] : __fsqrt_rn(key[1]));
+        }
+        return;
+    }
+    if (lane < k) {
+        idx[q * k + lane] = id[0] == INT32_MAX ? -1 : id[0];
+        dist[q * k + lane] = out_squared ? key[0] : (isinf(key[0]) ? key[0] : __fsqrt_rn(key[0]));
+    }
+}
+
+// ----------------------------------------------------------------------------- host
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+umap_status get_encode(EncodeTiledFn* fn)
+{
+    static EncodeTiledFn cached = nullptr;
+    if (!cached) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        UMAP_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) {
+            set_last_error("cuTensorMapEncodeTiled unavailable");
+            return UMAP_ERR_CUDA;
+        }
+        cached = (EncodeTiledFn)p;
+    }
+    *fn = cached;
+    return UMAP_OK;
+}
+
+umap_status make_map(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, int d_pad, int box_rows)
+{
+    EncodeTiledFn enc;
+    UMAP_TRY(get_encode(&enc));
+    cuuint64_t dims[2] = {(cuuint64_t)d_pad, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d_pad * 2};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_last_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        return UMAP_ERR_CUDA;
+    }
+    return UMAP_OK;
+}
+
+// centred BF16 copy + norms of X (rows n) with the given column mean (colsum / n_mean)
+umap_status prep_bf16(const float* X, int64_t n, int d, int d_pad, const double* colsum, int64_t n_mean,
+                      __nv_bfloat16* Xc, float* norms, cudaStream_t s)
+{
+    if (n == 0) return UMAP_OK;
+    center_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum, 1.0 / (double)n_mean, Xc, norms);
+    UMAP_LAUNCH_CHECK("center_bf16_kernel");
+    return UMAP_OK;
+}
+
+}  // namespace
+
+template <int KC, int ST>
+size_t knn_tc_smem_bytes() { return 1024 + ST * STAGE_BYTES + 8 * (2 * ST + 4) + 16; }
+
+template <int KC, int ST>
+umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
+{
+    const size_t smem = knn_tc_smem_bytes<KC, ST>();
+    static bool configured = false;
+    if (!configured) {
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        configured = true;
+    }
+    knn_tc_kernel<KC, ST><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
+    UMAP_LAUNCH_CHECK("knn_tc_kernel");
+    return UMAP_OK;
+}
+
+// Tensor-core candidate kNN + exact re-rank.  Centring uses the column means of the
+// reference set (R3).  kc = candidates per row (k <= kc <= 32).
+umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
+                       int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
+                       float* dist, cudaStream_t s)
+{
+    if (nq == 0) return UMAP_OK;
+    kc = std::min(TC_KCMAX, std::max(kc, 2 * k));
+    if (k >= TC_KCMAX) {
+        set_last_error("tensor kNN supports k < 64");
+        return UMAP_ERR_K_OUT_OF_RANGE;
+    }
+    if (nr >= (int64_t)INT32_MAX || nq >= (int64_t)INT32_MAX) {
+        set_last_error("tensor kNN: row count exceeds the TMA coordinate range");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
+    const bool same = (Xq == Xr && nq == nr);
+    Scratch colsum, xr16, rn, xq16, qn;
+    UMAP_TRY(colsum.alloc(sizeof(double) * d, s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(colsum.p, 0, sizeof(double) * d, s));
+    {
+        dim3 grid(ceil_div(d, 32), (unsigned)std::min<int64_t>(std::max<int64_t>(1, nr / 64), 512));
+        colsum_kernel<<<grid, 256, 0, s>>>(Xr, nr, d, colsum.as<double>());
+        UMAP_LAUNCH_CHECK("colsum_kernel");
+    }
+    UMAP_TRY(xr16.alloc(sizeof(__nv_bfloat16) * (size_t)nr * d_pad, s));
+    UMAP_TRY(rn.alloc(sizeof(float) * (size_t)nr, s));
+    UMAP_TRY(prep_bf16(Xr, nr, d, d_pad, colsum.as<double>(), nr, xr16.as<__nv_bfloat16>(), rn.as<float>(), s));
+    const __nv_bfloat16* q16 = xr16.as<__nv_bfloat16>();
+    const float* qnp = rn.as<float>();
+    if (!same) {
+        UMAP_TRY(xq16.alloc(sizeof(__nv_bfloat16) * (size_t)nq * d_pad, s));
+        UMAP_TRY(qn.alloc(sizeof(float) * (size_t)nq, s));
+        UMAP_TRY(prep_bf16(Xq, nq, d, d_pad, colsum.as<double>(), nr, xq16.as<__nv_bfloat16>(), qn.as<float>(), s));
+        q16 = xq16.as<__nv_bfloat16>();
+        qnp = qn.as<float>();
+    }
+    CUtensorMap map_q, map_r;
+    UMAP_TRY(make_map(&map_q, q16, nq, d_pad, TC_BM));
+    UMAP_TRY(make_map(&map_r, xr16.as<__nv_bfloat16>(), nr, d_pad, TC_BN));
+
+    // reference splits so that the grid covers the GPU (split-R, like the exact kernel)
+    const int64_t qblocks = (nq + TC_BM - 1) / TC_BM;
+    int64_t splits = std::max<int64_t>(1, (num_sms() + qblocks - 1) / qblocks);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, nr / (4 * TC_BN)));
+    int64_t split_len = (nr + splits - 1) / splits;
+    split_len = (split_len + TC_BN - 1) / TC_BN * TC_BN;
+    const int n_splits = (int)((nr + split_len - 1) / split_len);
+
+    Scratch ci, cd;
+    UMAP_TRY(ci.alloc(sizeof(int32_t) * (size_t)n_splits * nq * kc, s));
+    UMAP_TRY(cd.alloc(sizeof(float) * (size_t)n_splits * nq * kc, s));
+    TcArgs a{};
+    a.qnorm = qnp; a.rnorm = rn.as<float>(); a.nq = nq; a.nr = nr; a.kblocks = d_pad / TC_BK; a.kc = kc;
+    a.split_len = split_len; a.self_shift = self_shift; a.exclude_self = exclude_self;
+    a.index_offset = index_offset; a.cand_idx = ci.as<int32_t>(); a.cand_d2 = cd.as<float>();
+    {
+        const char* dbg = getenv("UMAP_TC_DEBUG");
+        a.debug = dbg ? atoi(dbg) : 0;
+    }
+    const dim3 grid((unsigned)qblocks, n_splits);
+    if (kc <= 32) UMAP_TRY((launch_tc<32, 4>(map_q, map_r, a, grid, s)));
+    else UMAP_TRY((launch_tc<64, 4>(map_q, map_r, a, grid, s)));
+    const int32_t* cand = ci.as<int32_t>();
+    Scratch mi, md;
+    if (n_splits > 1) {  // merge the per-split candidate lists by approximate key
+        UMAP_TRY(mi.alloc(sizeof(int32_t) * (size_t)nq * kc, s));
+        UMAP_TRY(md.alloc(sizeof(float) * (size_t)nq * kc, s));
+        UMAP_TRY(topk_merge(ci.as<int32_t>(), cd.as<float>(), n_splits, nq, kc, kc, 1, mi.as<int32_t>(),
+                            md.as<float>(), s));
+        cand = mi.as<int32_t>();
+    }
+    rerank_kernel<<<ceil_div(nq * 32, 256), 256, 0, s>>>(Xq, Xr, d, nq, cand, kc, index_offset, k, out_squared, idx,
+                                                         dist);
+    UMAP_LAUNCH_CHECK("rerank_kernel");
+    return UMAP_OK;
 }
 
 }  // namespace umapb200

@@ -103,6 +103,47 @@ def test_knn_split_reference_and_topk_merge(O):
     assert np.array_equal(np_(mi), ri) and np.array_equal(np_(md), rd)
 
 
+# tensor-core candidate mode (R3): recall >= 0.999 against the exact oracle, and rows whose
+# candidate set covers the truth are bit-identical to the exact mode
+TC_CASES = [
+    (1000, 50, 15, "lowrank"),
+    (2000, 784, 15, "lowrank"),
+    (1500, 100, 15, "iso"),
+    (700, 3072, 15, "lowrank"),
+    (300, 8, 5, "lowrank"),
+    (1300, 64, 32, "lowrank"),
+    (600, 3, 15, "ties"),
+]
+
+
+def _recall(gi, ri):
+    return np.mean([len(set(a) & set(b)) / len(b) for a, b in zip(gi, ri)])
+
+
+@pytest.mark.parametrize("n,d,k,kind", TC_CASES)
+def test_knn_tensor_recall_and_exactness(O, n, d, k, kind):
+    X = _data(kind, n, d, seed=11)
+    ri, rd = O.knn(X, X, k, self_offset=0)
+    gi, gd = U.knn(cu(X), cu(X), k, exclude_self=True, mode="tensor")
+    gi, gd = np_(gi), np_(gd)
+    assert _recall(gi, ri) >= 0.999
+    same = np.array([set(a) == set(b) for a, b in zip(gi, ri)])
+    assert np.array_equal(gi[same], ri[same])
+    assert np.array_equal(gd[same], rd[same])
+
+
+def test_knn_tensor_query_set_offsets_and_splits(O):
+    X = synth.lowrank(5000, 96, seed=12)
+    Xq, Xr = X[:37], X[37:]
+    ri, rd = O.knn(Xq, Xr, 15)
+    gi, gd = U.knn(cu(Xq), cu(Xr), 15, index_offset=500, mode="tensor")
+    assert _recall(np_(gi) - 500, ri) >= 0.999
+    # shard of a self-kNN: queries are global rows 0..36, references global rows 37..4999
+    ri2, _ = O.knn(X[:37], X, 15, self_offset=0)
+    gi2, _ = U.knn(cu(X[:37]), cu(X), 15, exclude_self=True, mode="tensor")
+    assert _recall(np_(gi2), ri2) >= 0.999
+
+
 def test_knn_empty_query_and_errors():
     X = cu(synth.lowrank(50, 4))
     gi, gd = U.knn(X[:0], X, 5)
