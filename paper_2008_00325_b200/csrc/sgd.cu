@@ -17,6 +17,8 @@
 //    its head in registers through the attractive and the m repulsive updates
 //    (the paper's register accumulation) and pushes -g_att to the tail and
 //    the accumulated head delta with fp32 vector atomics.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace umapb200 {
@@ -25,16 +27,17 @@ namespace {
 
 struct SgdArgs {
     const int64_t* indptr;
-    const int32_t* col;
-    const float* val;
-    const float* w_max;      // device scalar
+    const int2* edges;       // per CSR entry {col, float_as_int(r)}, r = w / w_max (R9), built once
     int64_t n;
-    const float* Yr;         // positions read (Y_e)
-    float* Yw;               // positions written (Y_{e+1}, or == Yr in Hogwild)
+    int64_t n_chunks;        // ceil(n / VPW)
+    float* Y0;               // positions (Hogwild: in place)
+    float* Y1;               // deterministic: ping-pong partner of Y0
     float a, b, gamma, alpha0;
-    int32_t n_epochs, epoch, m;
+    int32_t n_epochs, e_begin, e_end, m;
     uint32_t key0, key1;
-    unsigned long long* positives;  // optional device counter
+    unsigned long long* positives;  // device counter of due directed edges
+    unsigned int* bar;       // grid barrier {count, generation}
+    int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only
 };
 
 __device__ __forceinline__ float clip4(float v) { return fminf(fmaxf(v, -4.0f), 4.0f); }
@@ -47,32 +50,75 @@ __device__ __forceinline__ bool edge_due(float r, int e)
     return floorf(__fmul_rn((float)e, r)) > floorf(__fmul_rn((float)(e - 1), r));
 }
 
+// positions are read through L2 only (ld.global.cg): they change between epochs of the
+// persistent kernel and L1 is not coherent
 template <int DIM>
 __device__ __forceinline__ void load_row(const float* Y, int64_t v, float (&y)[DIM])
 {
     if (DIM == 2) {
-        const float2 t = *reinterpret_cast<const float2*>(Y + v * 2);
+        const float2 t = __ldcg(reinterpret_cast<const float2*>(Y + v * 2));
         y[0] = t.x; y[1] = t.y;
     } else if (DIM == 4) {
-        const float4 t = *reinterpret_cast<const float4*>(Y + v * 4);
+        const float4 t = __ldcg(reinterpret_cast<const float4*>(Y + v * 4));
         y[0] = t.x; y[1] = t.y; y[2] = t.z; y[3] = t.w;
     } else {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) y[c] = Y[v * DIM + c];
+        for (int c = 0; c < DIM; ++c) y[c] = __ldcg(Y + v * DIM + c);
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ void load_row_ro(const float* Y, int64_t v, float (&y)[DIM])
+{
+    if (DIM == 2) {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(Y + v * 2));
+        y[0] = t.x; y[1] = t.y;
+    } else if (DIM == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(Y + v * 4));
+        y[0] = t.x; y[1] = t.y; y[2] = t.z; y[3] = t.w;
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) y[c] = __ldg(Y + v * DIM + c);
     }
 }
 
 constexpr int SGD_WARPS = 8;
 constexpr int QCAP = 64;
 
-// Process one due edge (h, t): returns the head delta (deterministic: in fixed point).
-template <int DIM, bool DET>
-__device__ __forceinline__ void process_edge(const SgdArgs& A, float alpha, int64_t h, int64_t t,
-                                             long long (&qacc)[DIM])
+// R13 fixed point: q(g) = round(g 2^24) (exact scaling, |g| <= 4 so |q| <= 2^26 fits int32)
+__device__ __forceinline__ int qfix(float g) { return __float2int_rn(g * 16777216.0f); }
+
+// One due edge (h, t) at epoch e: attractive update of h (and, Hogwild, t) and M negative
+// samples on h.  MC = compile-time M (all negative-sample loads issued before use), or 0
+// for a runtime M.  DET: the head contribution is returned in fixed point (qacc); the
+// tail contribution is the head contribution of (t, h), computed by t's owner.
+template <int DIM, bool DET, int MC>
+__device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, float* Yw, int epoch, float alpha,
+                                             int h, int t, int (&qacc)[DIM])
 {
     float yh[DIM], yt[DIM], g[DIM];
-    load_row<DIM>(A.Yr, h, yh);
-    load_row<DIM>(A.Yr, t, yt);
+    constexpr int MP = MC > 0 ? MC : 1;
+    int vv[MP];
+    float yv[MP][DIM];
+    if (MC > 0) {
+        // Philox counter (h, t, e, p>>2) (R11) first, then the head, tail and all M sample
+        // rows are requested together: one L2 round trip per due edge
+#pragma unroll
+        for (int blk = 0; blk < (MP + 3) / 4; ++blk) {
+            const u32x4 rnd = philox4x32_10((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)blk, A.key0, A.key1);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int p = 4 * blk + i;
+                if (p < MP) vv[p] = (int)__umulhi(pick(rnd, i), (uint32_t)A.n);
+            }
+        }
+    }
+    load_row<DIM>(Yr, h, yh);
+    load_row<DIM>(Yr, t, yt);
+    if (MC > 0) {
+#pragma unroll
+        for (int p = 0; p < MP; ++p) load_row<DIM>(Yr, vv[p], yv[p]);
+    }
     float s = 0.0f;
 #pragma unroll
     for (int c = 0; c < DIM; ++c) { const float df = yh[c] - yt[c]; s = fmaf(df, df, s); }
@@ -86,42 +132,49 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, float alpha, int6
     float h0[DIM];
     if (DET) {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) qacc[c] += 2 * __double2ll_rn((double)g[c] * 4294967296.0);
+        for (int c = 0; c < DIM; ++c) qacc[c] += 2 * qfix(g[c]);
     } else {
 #pragma unroll
         for (int c = 0; c < DIM; ++c) { h0[c] = yh[c]; yh[c] += g[c]; }
         if (DIM == 2) {
-            atomicAdd(reinterpret_cast<float2*>(A.Yw + t * 2), make_float2(-g[0], -g[1]));
+            atomicAdd(reinterpret_cast<float2*>(Yw + t * 2), make_float2(-g[0], -g[1]));
         } else {
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) atomicAdd(A.Yw + t * DIM + c, -g[c]);
+            for (int c = 0; c < DIM; ++c) atomicAdd(Yw + t * DIM + c, -g[c]);
         }
     }
-    // m negative samples, head only; Philox counter (h, t, e, p>>2) (R11)
+    const int pend = MC > 0 ? MC : A.m;
     u32x4 rnd = {0, 0, 0, 0};
-    for (int p = 0; p < A.m; ++p) {
-        if ((p & 3) == 0)
-            rnd = philox4x32_10((uint32_t)h, (uint32_t)t, (uint32_t)A.epoch, (uint32_t)(p >> 2), A.key0, A.key1);
-        const uint32_t u = pick(rnd, p & 3);
-        const int64_t v = (int64_t)(((unsigned long long)u * (unsigned long long)A.n) >> 32);
+#pragma unroll
+    for (int p = 0; p < pend; ++p) {
+        int v;
+        float yvv[DIM];
+        if (MC > 0) {
+            v = vv[MC > 0 ? p : 0];
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) yvv[c] = yv[MC > 0 ? p : 0][c];
+        } else {
+            if ((p & 3) == 0)
+                rnd = philox4x32_10((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)(p >> 2), A.key0, A.key1);
+            v = (int)__umulhi(pick(rnd, p & 3), (uint32_t)A.n);
+            load_row<DIM>(Yr, v, yvv);
+        }
         if (v == h) continue;
-        float yv[DIM];
-        load_row<DIM>(A.Yr, v, yv);
         float s2 = 0.0f;
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) { const float df = yh[c] - yv[c]; s2 = fmaf(df, df, s2); }
+        for (int c = 0; c < DIM; ++c) { const float df = yh[c] - yvv[c]; s2 = fmaf(df, df, s2); }
         if (s2 > 0.0f) {
             const float sb = pow_b(s2, A.b);
             const float cr = __fdividef(2.0f * A.gamma * A.b, (0.001f + s2) * fmaf(A.a, sb, 1.0f));
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) g[c] = clip4(cr * (yh[c] - yv[c])) * alpha;
+            for (int c = 0; c < DIM; ++c) g[c] = clip4(cr * (yh[c] - yvv[c])) * alpha;
         } else {
 #pragma unroll
             for (int c = 0; c < DIM; ++c) g[c] = 4.0f * alpha;
         }
         if (DET) {
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) qacc[c] += __double2ll_rn((double)g[c] * 4294967296.0);
+            for (int c = 0; c < DIM; ++c) qacc[c] += qfix(g[c]);
         } else {
 #pragma unroll
             for (int c = 0; c < DIM; ++c) yh[c] += g[c];
@@ -129,98 +182,159 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, float alpha, int6
     }
     if (!DET) {
         if (DIM == 2) {
-            atomicAdd(reinterpret_cast<float2*>(A.Yw + h * 2), make_float2(yh[0] - h0[0], yh[1] - h0[1]));
+            atomicAdd(reinterpret_cast<float2*>(Yw + h * 2), make_float2(yh[0] - h0[0], yh[1] - h0[1]));
         } else {
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) atomicAdd(A.Yw + h * DIM + c, yh[c] - h0[c]);
+            for (int c = 0; c < DIM; ++c) atomicAdd(Yw + h * DIM + c, yh[c] - h0[c]);
         }
     }
 }
 
-template <int DIM, bool DET>
-__global__ void __launch_bounds__(32 * SGD_WARPS) sgd_epoch_kernel(SgdArgs A)
+// grid-wide barrier between epochs (cooperative launch guarantees co-residency);
+// the gpu-scope fences order the epoch's writes and invalidate L1
+__device__ __forceinline__ void grid_barrier(unsigned int* bar)
 {
-    __shared__ int32_t q_h[SGD_WARPS][QCAP];   // local owner lane of the queued edge
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* gen = bar + 1;
+        const unsigned int my = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == my) { __nanosleep(32); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Persistent SGD: epochs [e_begin, e_end) in one cooperative launch.  A warp work unit
+// owns VPW consecutive vertices; their CSR rows are contiguous, so the warp streams the
+// (col, r) records with coalesced loads, evaluates the closed-form schedule (R9), and
+// compacts due edges into a per-warp queue that is processed 32 at a time (every lane
+// carries a due edge during the expensive part).
+template <int DIM, bool DET, int MC, int VPW, int MINB>
+__global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(SgdArgs A)
+{
+    __shared__ int32_t q_h[SGD_WARPS][QCAP];   // owner lane (0..VPW-1) of the queued edge
     __shared__ int32_t q_t[SGD_WARPS][QCAP];   // tail vertex
-    __shared__ long long acc[SGD_WARPS][DIM][32];
-    __shared__ int64_t ptr_s[SGD_WARPS][33];
+    __shared__ long long acc[SGD_WARPS][DIM][VPW];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t v0 = ((int64_t)blockIdx.x * SGD_WARPS + warp) * 32;
-    if (v0 >= A.n) return;
-    const int nv = (int)imin64(32, A.n - v0);
-    ptr_s[warp][lane] = A.indptr[v0 + min(lane, nv)];
-    if (lane == 0) ptr_s[warp][32] = A.indptr[v0 + nv];
-#pragma unroll
-    for (int c = 0; c < DIM; ++c) acc[warp][c][lane] = 0;
-    __syncwarp();
-    const int64_t e_begin = ptr_s[warp][0], e_end = ptr_s[warp][32];
-    const float w_max = *A.w_max;
-    const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)A.epoch, (float)A.n_epochs)));
-    int qn = 0;
+    const int n = (int)A.n;
+    const int n_chunks = (int)A.n_chunks;
     unsigned long long due_count = 0;
-
-    auto drain = [&](int count) {
-        // lanes < count take one queued item each
-        if (lane < count) {
-            const int hl = q_h[warp][lane];
-            long long qa[DIM];
+    for (int epoch = A.e_begin; epoch < A.e_end; ++epoch) {
+        const int par = (epoch - A.e_begin) & 1;
+        const float* Yr = (DET && par) ? A.Y1 : A.Y0;
+        float* Yw = DET ? (par ? A.Y0 : A.Y1) : A.Y0;
+        const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
+        const int wid = blockIdx.x * SGD_WARPS + warp, nw = gridDim.x * SGD_WARPS;
+        for (int chunk = wid; chunk < (A.debug & 1 ? 0 : n_chunks); chunk += nw) {  // static round-robin (a shared
+            // work counter serialises at L2: thousands of grabs per epoch)
+            const int v0 = chunk * VPW;
+            const int nv = min(VPW, n - v0);
+            // lane l < nv holds indptr[v0 + l]; the end is loaded separately (nv may be 32)
+            const int64_t ptr_l = lane < nv ? __ldg(A.indptr + v0 + lane) : 0;
+            const int64_t e_lo = __shfl_sync(0xffffffffu, ptr_l, 0);
+            const int64_t e_hi = __ldg(A.indptr + v0 + nv);
+            const int32_t pr = (int32_t)(ptr_l - e_lo);   // row offsets relative to the chunk
+            if (DET && lane < VPW) {
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) qa[c] = 0;
-            process_edge<DIM, DET>(A, alpha, v0 + hl, (int64_t)q_t[warp][lane], qa);
-            if (DET) {
+                for (int c = 0; c < DIM; ++c) acc[warp][c][lane] = 0;
+            }
+            __syncwarp();
+            int qn = 0;
+            auto drain = [&](int count) {
+                const bool act = lane < count;
+                const int hl = act ? q_h[warp][lane] : -1;
+                int qa[DIM];
 #pragma unroll
-                for (int c = 0; c < DIM; ++c)
-                    atomicAdd(reinterpret_cast<unsigned long long*>(&acc[warp][c][hl]), (unsigned long long)qa[c]);
+                for (int c = 0; c < DIM; ++c) qa[c] = 0;
+                if (act) process_edge<DIM, DET, MC>(A, Yr, Yw, epoch, alpha, v0 + hl, q_t[warp][lane], qa);
+                if (DET) {
+                    // queued items are in CSR order, so equal owners are contiguous: segmented
+                    // sum over the warp, the last lane of each segment adds it (order-free int sum)
+                    long long sv[DIM];
+#pragma unroll
+                    for (int c = 0; c < DIM; ++c) sv[c] = qa[c];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int ho = __shfl_up_sync(0xffffffffu, hl, o);
+#pragma unroll
+                        for (int c = 0; c < DIM; ++c) {
+                            const long long so = __shfl_up_sync(0xffffffffu, sv[c], o);
+                            if (lane >= o && ho == hl) sv[c] += so;
+                        }
+                    }
+                    const int hn = __shfl_down_sync(0xffffffffu, hl, 1);
+                    if (act && (lane == count - 1 || hn != hl)) {
+#pragma unroll
+                        for (int c = 0; c < DIM; ++c) acc[warp][c][hl] += sv[c];
+                    }
+                }
+                __syncwarp();
+            };
+            int2 nrec = (e_lo + lane < e_hi) ? __ldg(A.edges + e_lo + lane) : make_int2(0, 0);
+            for (int64_t base = e_lo; base < e_hi; base += 32) {
+                const int64_t e = base + lane;
+                const int32_t el = (int32_t)(e - e_lo);
+                const int2 rec = nrec;  // records are prefetched one 32-edge step ahead
+                if (base + 32 + lane < e_hi) nrec = __ldg(A.edges + base + 32 + lane);
+                const bool due = e < e_hi && edge_due(__int_as_float(rec.y), epoch);
+                // owner lane: largest l < nv with pr[l] <= el (shuffle binary search)
+                int lo = 0, hi = nv;
+#pragma unroll
+                for (int it = 0; it < (VPW > 16 ? 5 : (VPW > 8 ? 4 : 3)); ++it) {
+                    const int mid = (lo + hi) >> 1;
+                    const int32_t pm = __shfl_sync(0xffffffffu, pr, mid);
+                    if (hi - lo > 1) { if (pm <= el) lo = mid; else hi = mid; }
+                }
+                const unsigned ballot = __ballot_sync(0xffffffffu, due);
+                due_count += __popc(ballot);
+                if (due) {
+                    const int pos = qn + __popc(ballot & ((1u << lane) - 1u));
+                    q_h[warp][pos] = lo;
+                    q_t[warp][pos] = rec.x;
+                }
+                __syncwarp();
+                qn += __popc(ballot);
+                if (qn >= 32) {
+                    drain(32);
+                    qn -= 32;
+                    if (lane < qn) {
+                        q_h[warp][lane] = q_h[warp][32 + lane];
+                        q_t[warp][lane] = q_t[warp][32 + lane];
+                    }
+                    __syncwarp();
+                }
             }
-        }
-        __syncwarp();
-    };
-
-    for (int64_t base = e_begin; base < e_end; base += 32) {
-        const int64_t e = base + lane;
-        bool due = false;
-        int32_t tail = 0, hl = 0;
-        if (e < e_end) {
-            const float r = __fdiv_rn(A.val[e], w_max);
-            due = edge_due(r, A.epoch);
-            tail = A.col[e];
-            // owner lane: largest l with ptr_s[l] <= e (binary search over 33 offsets)
-            int lo = 0, hi = nv;  // invariant ptr[lo] <= e < ptr[hi]
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (ptr_s[warp][mid] <= e) lo = mid; else hi = mid;
-            }
-            hl = lo;
-        }
-        const unsigned ballot = __ballot_sync(0xffffffffu, due);
-        due_count += __popc(ballot);
-        if (due) {
-            const int pos = qn + __popc(ballot & ((1u << lane) - 1u));
-            q_h[warp][pos] = hl;
-            q_t[warp][pos] = tail;
-        }
-        __syncwarp();
-        qn += __popc(ballot);
-        if (qn >= 32) {
-            drain(32);
-            qn -= 32;
-            if (lane < qn) {  // move the remainder to the front
-                q_h[warp][lane] = q_h[warp][32 + lane];
-                q_t[warp][lane] = q_t[warp][32 + lane];
+            if (qn > 0) drain(qn);
+            if (DET && lane < nv) {
+                const int v = v0 + lane;
+                float yo[DIM];
+                load_row<DIM>(Yr, v, yo);
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) {
+                    const double upd = (double)acc[warp][c][lane] * (1.0 / 16777216.0);
+                    Yw[(int64_t)v * DIM + c] = (float)((double)yo[c] + upd);
+                }
             }
             __syncwarp();
         }
+        if (epoch + 1 < A.e_end) grid_barrier(A.bar);
     }
-    if (qn > 0) drain(qn);
-    if (DET && lane < nv) {
-        const int64_t v = v0 + lane;
-#pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            const double upd = (double)acc[warp][c][lane] * (1.0 / 4294967296.0);
-            A.Yw[v * DIM + c] = (float)((double)A.Yr[v * DIM + c] + upd);
-        }
-    }
+    // due_count is warp-uniform (every lane added the same ballot counts)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
+__global__ void edge_records_kernel(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t nnz,
+                                    const float* __restrict__ w_max, int2* __restrict__ out)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nnz) out[e] = make_int2(col[e], __float_as_int(__fdiv_rn(val[e], *w_max)));
 }
 
 __global__ void wmax_kernel(const float* __restrict__ val, int64_t nnz, float* __restrict__ out)
@@ -343,14 +457,52 @@ transform_sgd_kernel(const int32_t* __restrict__ idx, const float* __restrict__ 
     for (int c = 0; c < DIM; ++c) Yq[q * DIM + c] = y[c];
 }
 
-template <int DIM>
-umap_status launch_epoch(const SgdArgs& A, bool det, cudaStream_t s)
+template <int DIM, bool DET, int MC, int VPW, int MINB>
+umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
 {
-    const unsigned grid = ceil_div(A.n, 32 * SGD_WARPS);
-    if (det) sgd_epoch_kernel<DIM, true><<<grid, 32 * SGD_WARPS, 0, s>>>(A);
-    else sgd_epoch_kernel<DIM, false><<<grid, 32 * SGD_WARPS, 0, s>>>(A);
-    UMAP_LAUNCH_CHECK("sgd_epoch_kernel");
+    auto kern = sgd_persistent_kernel<DIM, DET, MC, VPW, MINB>;
+    A.n_chunks = (A.n + VPW - 1) / VPW;
+    static int max_blocks = -1;
+    if (max_blocks < 0) {
+        int per_sm = 0;
+        UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * SGD_WARPS, 0));
+        max_blocks = std::max(1, per_sm) * num_sms();
+    }
+    const int64_t want = (A.n_chunks + SGD_WARPS - 1) / SGD_WARPS;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, max_blocks));
+    void* args[] = {&A};
+    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * SGD_WARPS), args, 0, s));
+    UMAP_LAUNCH_CHECK("sgd_persistent_kernel");
     return UMAP_OK;
+}
+
+int sgd_variant()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("UMAP_SGD_VARIANT");  // tuning knob: 0 = default
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int DIM, bool DET, int MC>
+umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
+{
+    switch (DIM == 2 ? sgd_variant() : 0) {
+        case 1: return launch_sgd_t<DIM, DET, MC, 16, 3>(A, s);
+        case 2: return launch_sgd_t<DIM, DET, MC, 8, 3>(A, s);
+        case 3: return launch_sgd_t<DIM, DET, MC, 32, 4>(A, s);
+        case 4: return launch_sgd_t<DIM, DET, MC, 16, 4>(A, s);
+        default: return launch_sgd_t<DIM, DET, MC, 32, 3>(A, s);
+    }
+}
+
+template <int DIM>
+umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
+{
+    if (A.m == 5) return det ? launch_sgd_m<DIM, true, 5>(A, s) : launch_sgd_m<DIM, false, 5>(A, s);
+    return det ? launch_sgd_m<DIM, true, 0>(A, s) : launch_sgd_m<DIM, false, 0>(A, s);
 }
 
 template <int DIM, int KMAX>
@@ -397,8 +549,7 @@ umap_status compute_wmax(const float* val, int64_t nnz, float* wmax_dev, cudaStr
     return UMAP_OK;
 }
 
-// Run epochs [e_begin, e_end) on Y (device, in place).  nnz_bound: an upper bound of
-// indptr[n] used only to size the w_max pass (the exact value is read from indptr).
+// Run epochs [e_begin, e_end) on Y (device, in place).  nnz = indptr[n].
 umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const float* val, int64_t n, int64_t nnz,
                             float* Y, const umap_params* p, int e_begin, int e_end, int64_t* positives_host,
                             cudaStream_t s)
@@ -410,42 +561,51 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
     }
     if (e_begin < 1) e_begin = 1;
     if (e_end > p->n_epochs) e_end = p->n_epochs;
-    Scratch wmax, other, counter;
+    if (positives_host) *positives_host = 0;
+    if (e_begin >= e_end || n == 0) return UMAP_OK;
+    if (n >= (int64_t)INT32_MAX) { set_last_error("n must be < 2^31"); return UMAP_ERR_INVALID_ARGUMENT; }
+    Scratch wmax, other, counter, edges, bar;
     UMAP_TRY(wmax.alloc(sizeof(float), s));
     UMAP_TRY(compute_wmax(val, nnz, wmax.as<float>(), s));
+    // a6: per-entry record {col, r = w / w_max}, built once per call
+    UMAP_TRY(edges.alloc(sizeof(int2) * (size_t)std::max<int64_t>(nnz, 1), s));
+    if (nnz > 0) {
+        edge_records_kernel<<<ceil_div(nnz, 256), 256, 0, s>>>(col, val, nnz, wmax.as<float>(), edges.as<int2>());
+        UMAP_LAUNCH_CHECK("edge_records_kernel");
+    }
     UMAP_TRY(counter.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), s));
+    const size_t bar_words = 2 + (size_t)(e_end - e_begin);
+    UMAP_TRY(bar.alloc(bar_words * sizeof(unsigned int), s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(bar.p, 0, bar_words * sizeof(unsigned int), s));
     const bool det = p->sgd_mode == UMAP_SGD_DETERMINISTIC;
-    float* bufs[2] = {Y, nullptr};
     if (det) {
         UMAP_TRY(other.alloc(sizeof(float) * (size_t)n * dim, s));
-        bufs[1] = other.as<float>();
     }
     SgdArgs A{};
-    A.indptr = indptr; A.col = col; A.val = val; A.w_max = wmax.as<float>(); A.n = n;
+    A.indptr = indptr; A.edges = edges.as<int2>(); A.n = n;
+    A.Y0 = Y; A.Y1 = det ? other.as<float>() : Y;
     A.a = p->a; A.b = p->b; A.gamma = p->repulsion_strength; A.alpha0 = p->learning_rate;
-    A.n_epochs = p->n_epochs; A.m = p->negative_sample_rate;
+    A.n_epochs = p->n_epochs; A.e_begin = e_begin; A.e_end = e_end; A.m = p->negative_sample_rate;
     A.key0 = (uint32_t)p->seed; A.key1 = (uint32_t)(p->seed >> 32);
     A.positives = counter.as<unsigned long long>();
-    int cur = 0;
-    for (int e = e_begin; e < e_end; ++e) {
-        A.epoch = e;
-        A.Yr = bufs[cur];
-        A.Yw = det ? bufs[cur ^ 1] : bufs[cur];
-        umap_status st;
-        switch (dim) {
-            case 1: st = launch_epoch<1>(A, det, s); break;
-            case 2: st = launch_epoch<2>(A, det, s); break;
-            case 3: st = launch_epoch<3>(A, det, s); break;
-            case 4: st = launch_epoch<4>(A, det, s); break;
-            case 8: st = launch_epoch<8>(A, det, s); break;
-            default: st = launch_epoch<16>(A, det, s); break;
-        }
-        if (st != UMAP_OK) return st;
-        if (det) cur ^= 1;
+    A.bar = bar.as<unsigned int>();
+    {
+        const char* dbg = getenv("UMAP_SGD_DEBUG");
+        A.debug = dbg ? atoi(dbg) : 0;
     }
-    if (cur != 0) {
-        UMAP_CUDA_TRY(cudaMemcpyAsync(Y, bufs[cur], sizeof(float) * (size_t)n * dim, cudaMemcpyDeviceToDevice, s));
+    umap_status st;
+    switch (dim) {
+        case 1: st = launch_sgd<1>(A, det, s); break;
+        case 2: st = launch_sgd<2>(A, det, s); break;
+        case 3: st = launch_sgd<3>(A, det, s); break;
+        case 4: st = launch_sgd<4>(A, det, s); break;
+        case 8: st = launch_sgd<8>(A, det, s); break;
+        default: st = launch_sgd<16>(A, det, s); break;
+    }
+    if (st != UMAP_OK) return st;
+    if (det && ((e_end - e_begin) & 1)) {  // odd number of epochs: the result sits in the partner buffer
+        UMAP_CUDA_TRY(cudaMemcpyAsync(Y, other.p, sizeof(float) * (size_t)n * dim, cudaMemcpyDeviceToDevice, s));
     }
     if (positives_host) {
         unsigned long long c = 0;

@@ -282,7 +282,7 @@ def test_fit_c1_digits_vs_oracle(O):
         Y, st = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=0, sgd_mode=mode)
         T, _ = U.trustworthiness(cu(X), Y, 15)
         assert abs(T - t_ref) <= 0.005, (mode, T, t_ref)
-        assert st["gpu_launches"] > 200 and st["nnz"] > 0
+        assert st["gpu_launches"] >= 10 and st["nnz"] > 0
 
 
 def test_fit_host_pointers_equal_device(O):
