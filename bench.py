@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--knn-mode", default="exact", choices=["exact", "tensor"])
+    ap.add_argument("--knn-mode", default="tensor", choices=["exact", "tensor"])
     ap.add_argument("--sgd-mode", default="deterministic", choices=["deterministic", "hogwild"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -220,10 +220,10 @@ def run_ours(args):
     def step(Xd):
         if world == 1:
             Y, st = U.fit(Xd, **kw)
-            T, S = U.trustworthiness(Xd, Y, trust_k)
+            T, S = U.trustworthiness(Xd, Y, trust_k, knn_mode=args.knn_mode)
         else:
             Y, st = D.sharded_fit(Xd, **kw)
-            T, S = D.sharded_trustworthiness(Xd, Y, trust_k)
+            T, S = D.sharded_trustworthiness(Xd, Y, trust_k, knn_mode=args.knn_mode)
         return Y, st, T
 
     def barrier():

@@ -139,7 +139,9 @@ UMAP_API umap_status umap_transform(const float* X_train, const float* Y_train, 
  * r_i(j) = 1 + #{l != i : (d2_X(i,l), l) < (d2_X(i,j), j)}.
  * X n x d, Y n x d_emb (host or device); T (host double), penalty (host int64,
  * optional NULL) = the integer sum.  Requires 1 <= k < n/2.
- * knn_mode: UMAP_KNN_EXACT_FP32 (only mode in this build; TENSOR -> UNSUPPORTED). */
+ * knn_mode: UMAP_KNN_EXACT_FP32 counts ranks in the exact fp32 distance kernel;
+ * UMAP_KNN_TENSOR_BF16 uses a split-BF16 tcgen05 GEMM whose error bound certifies most
+ * (row, reference) buckets and re-checks the rest exactly -- the same integer S either way. */
 UMAP_API umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int32_t d_emb, int64_t n,
                                  int32_t k, int32_t knn_mode, double* T, int64_t* penalty, void* stream);
 
@@ -204,11 +206,11 @@ UMAP_API umap_status umap_transform_optimize(const int32_t* idx, const float* w,
                                     int32_t e_end, int64_t q_offset, int32_t init, void* stream);
 
 /* a10 input-space rank penalties for rows [row_begin, row_end) (R16): emb_idx is the
- * embedding kNN of those rows (n_rows x k, global ids).  row_pen: n_rows int64
- * (optional NULL); *penalty (host) = sum. */
+ * embedding kNN of those rows (n_rows x k, global ids).  knn_mode as in
+ * umap_trustworthiness.  row_pen: n_rows int64 (optional NULL); *penalty (host) = sum. */
 UMAP_API umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
-                               int64_t row_begin, int64_t row_end, int64_t* row_pen, int64_t* penalty,
-                               void* stream);
+                               int64_t row_begin, int64_t row_end, int32_t knn_mode, int64_t* row_pen,
+                               int64_t* penalty, void* stream);
 
 UMAP_API const char* umap_status_string(umap_status s);
 UMAP_API const char* umap_last_error(void);

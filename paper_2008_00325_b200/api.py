@@ -215,7 +215,7 @@ def transform_optimize(idx, w, Y_train, Yq, n_epochs_t, e_begin=1, e_end=None, q
     return Yq
 
 
-def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None):
+def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None, knn_mode="exact"):
     X = _dev(X, torch.float32, "X")
     emb_idx = _dev(emb_idx, torch.int32, "emb_idx")
     n = X.shape[0]
@@ -223,7 +223,8 @@ def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None):
         row_end = n
     pen = torch.empty(row_end - row_begin, dtype=torch.int64, device=X.device)
     S = ctypes.c_int64()
-    check(_lib.load().umap_trust_penalty(_ptr(X), n, X.shape[1], _ptr(emb_idx), k, row_begin, row_end, _ptr(pen),
+    check(_lib.load().umap_trust_penalty(_ptr(X), n, X.shape[1], _ptr(emb_idx), k, row_begin, row_end,
+                                         KNN_MODES[knn_mode], _ptr(pen),
                                          ctypes.byref(S), _stream(X.device)), "umap_trust_penalty")
     return S.value, pen
 

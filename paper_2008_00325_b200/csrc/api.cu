@@ -31,7 +31,7 @@ umap_status transform_optimize(const int32_t* idx, const float* w, int64_t nq, i
                                float* Yq, const umap_params* p, int n_epochs_t, int e_begin, int e_end,
                                int64_t q_offset, int init, cudaStream_t s);
 umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
-                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, cudaStream_t s);
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, cudaStream_t s);
 bool dim_supported(int dim);
 
 // ---- error state
@@ -471,7 +471,8 @@ umap_status umap_transform_optimize(const int32_t* idx, const float* w, int64_t 
 }
 
 umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
-                               int64_t row_begin, int64_t row_end, int64_t* row_pen, int64_t* penalty, void* stream)
+                               int64_t row_begin, int64_t row_end, int32_t knn_mode, int64_t* row_pen,
+                               int64_t* penalty, void* stream)
 {
     UMAP_TRY(require_cuda());
     cudaStream_t s = (cudaStream_t)stream;
@@ -482,7 +483,7 @@ umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32
     UMAP_TRY(require_device(X, "X"));
     UMAP_TRY(require_device(emb_idx, "emb_idx"));
     UMAP_TRY(require_device(row_pen, "row_pen"));
-    UMAP_TRY(trust_penalty(X, n, d, emb_idx, k, row_begin, row_end, row_pen, penalty, s));
+    UMAP_TRY(trust_penalty(X, n, d, emb_idx, k, row_begin, row_end, row_pen, penalty, knn_mode, s));
     return UMAP_OK;
 }
 
@@ -656,7 +657,10 @@ umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int3
     cudaStream_t s = (cudaStream_t)stream;
     if (!X || !Y || !T || d < 1 || d_emb < 1) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
     if (k < 1 || k > 64 || 2 * (int64_t)k >= n) { set_last_error("1 <= k < n/2, k <= 64"); return UMAP_ERR_K_OUT_OF_RANGE; }
-    if (knn_mode != UMAP_KNN_EXACT_FP32) { set_last_error("trust: only exact fp32 mode"); return UMAP_ERR_UNSUPPORTED; }
+    if (knn_mode != UMAP_KNN_EXACT_FP32 && knn_mode != UMAP_KNN_TENSOR_BF16) {
+        set_last_error("unknown knn_mode");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
     DevIn Xd, Yd;
     UMAP_TRY(Xd.make(X, (size_t)n * d, s));
     UMAP_TRY(Yd.make(Y, (size_t)n * d_emb, s));
@@ -665,7 +669,7 @@ umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int3
     UMAP_TRY(edist.alloc(sizeof(float) * (size_t)n * k, s));
     UMAP_TRY(knn_exact(Yd.p, n, Yd.p, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
     int64_t S = 0;
-    UMAP_TRY(trust_penalty(Xd.p, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, s));
+    UMAP_TRY(trust_penalty(Xd.p, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, s));
     const double nn = (double)n, kk = (double)k;
     *T = 1.0 - (2.0 / (nn * kk * (2.0 * nn - 3.0 * kk - 1.0))) * (double)S;
     if (penalty) *penalty = S;

@@ -21,11 +21,14 @@
 //     mode bit for bit.
 #include <cuda.h>
 #include <cstdlib>
+#include <vector>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
 
 namespace umapb200 {
+
+static int64_t g_last_rank_ambiguous = 0;
 
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
                        int out_squared, int32_t* idx, float* dist, cudaStream_t s);
@@ -146,9 +149,19 @@ struct TcArgs {
     int debug;              // bit0: skip epilogue filtering, bit1: skip MMA issue (profiling only)
     int32_t* cand_idx;      // [split][n_q][kc]
     float* cand_d2;
+    // RANK mode (trustworthiness, R16)
+    const float* thr_d2;    // [n_q][k] exact sorted thresholds
+    int k;
+    float margin;           // c: |d2~ - d2_exact| < c (|q|^2 + |r|^2)
+    int32_t* hist;          // [n_q][k] certain bucket counts (written, not accumulated)
+    int2* amb;              // per-CTA regions of (query row, reference row) pairs to re-check
+    int amb_cap;            // capacity per CTA region
+    int* amb_count;         // [gridDim.x] entries used per CTA (may exceed cap -> overflow)
 };
 
-template <int KC, int TC_STAGES>
+constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
+
+template <int KC, int TC_STAGES, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_r, TcArgs a)
 {
@@ -235,6 +248,106 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 umma_commit(tfull0 + 8 * b);      // accumulator b complete
             }
         }
+    } else if constexpr (MODE == 1) {
+        // ---------------------------------------------------- RANK epilogue (warps 2..9)
+        // Trustworthiness input-space ranks (R16).  Thread = query row, its half of the
+        // columns.  d2~ approximates the exact R2 value within E = c (|q|^2 + |r|^2); a
+        // reference row below threshold t certainly iff d2~ + E < thr_t, certainly not iff
+        // d2~ - E > thr_t.  Rows whose bucket is certain are counted in a shared histogram;
+        // the rest are appended (warp-aggregated) for an exact re-check.
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quad * 32 + lane;
+        const int64_t q = q0 + row;
+        const bool valid = q < a.nq;
+        const float qn = valid ? a.qnorm[q] : 0.0f;
+        const int64_t self_j = (valid && a.exclude_self) ? q + a.self_shift : -1;
+        const int k = a.k;
+        float thr[TC_KT];
+#pragma unroll
+        for (int t = 0; t < TC_KT; ++t) thr[t] = (valid && t < k) ? a.thr_d2[q * k + t] : INFINITY;
+        const float thr_max = valid ? thr[0] : -INFINITY;
+        float tmax = thr_max;
+#pragma unroll
+        for (int t = 1; t < TC_KT; ++t) tmax = (t < k) ? thr[t] : tmax;
+        const float c_m = a.margin;
+        // shared histogram [half][t][row] after the ring region (ring stays untouched)
+        int32_t* Hs = reinterpret_cast<int32_t*>(stage_base + TC_STAGES * STAGE_BYTES + 8 * (2 * TC_STAGES + 4) + 16);
+        int* s_amb = reinterpret_cast<int*>(Hs + 2 * TC_KT * TC_BM);
+#pragma unroll
+        for (int t = 0; t < TC_KT; ++t) Hs[(half * TC_KT + t) * TC_BM + row] = 0;
+        if (warp == 2 && lane == 0) *s_amb = 0;
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+        int2* amb_base = a.amb + (int64_t)blockIdx.x * a.amb_cap;
+        for (int t = 0; t < ntiles; ++t) {
+            const int b = t & 1;
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
+            tc_fence_after();
+            const int64_t rb = r_lo + (int64_t)t * TC_BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
+#pragma unroll 1
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2); c += 32) {
+                float v[32];
+                tmem_ld32(taddr + c, v);
+                const int64_t jb = rb + c;
+                const float rn_l = (jb + lane < r_hi) ? __ldg(a.rnorm + jb + lane) : INFINITY;
+                uint32_t cm = 0;  // columns possibly below the largest threshold
+#pragma unroll
+                for (int u = 0; u < 32; ++u) {
+                    const float rn = __shfl_sync(0xffffffffu, rn_l, u);
+                    const float sq = qn + rn;
+                    v[u] = fmaf(-2.0f, v[u], sq);
+                    cm |= (uint32_t)(v[u] - c_m * sq < tmax) << u;
+                }
+                if (!valid) cm = 0;
+                if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
+                while (__any_sync(0xffffffffu, cm != 0)) {
+                    const int u = cm ? __ffs(cm) - 1 : 0;
+                    const bool has = cm != 0;
+                    cm &= cm - 1;
+                    float w16[16], w8[8], w4[4], w2[2];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) w16[i] = (u & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) w8[i] = (u & 2) ? w16[2 * i + 1] : w16[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) w4[i] = (u & 4) ? w8[2 * i + 1] : w8[2 * i];
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) w2[i] = (u & 8) ? w4[2 * i + 1] : w4[2 * i];
+                    const float d2a = (u & 16) ? w2[1] : w2[0];
+                    const float rn = __shfl_sync(0xffffffffu, rn_l, u);
+                    const float E = c_m * (qn + rn);
+                    const float hiv = d2a + E, lov = d2a - E;
+                    int b_hi = 0, b_lo = 0;  // #thresholds <= d2~ + E, <= d2~ - E
+#pragma unroll
+                    for (int tt = 0; tt < TC_KT; ++tt) {
+                        b_hi += thr[tt] <= hiv;
+                        b_lo += thr[tt] <= lov;
+                    }
+                    const bool amb = has && b_hi != b_lo;
+                    if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
+                    const unsigned am = __ballot_sync(0xffffffffu, amb);
+                    if (am) {
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(s_amb, __popc(am));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        if (amb) {
+                            const int pos = base + __popc(am & ((1u << lane) - 1u));
+                            if (pos < a.amb_cap) amb_base[pos] = make_int2((int)q, (int)(jb + u));
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+        if (half == 0 && valid) {
+            for (int t = 0; t < k; ++t)
+                a.hist[q * k + t] = Hs[t * TC_BM + row] + Hs[(TC_KT + t) * TC_BM + row];
+        }
+        if (warp == 2 && lane == 0) a.amb_count[blockIdx.x] = *s_amb;
     } else {
         // ---------------------------------------------------- epilogue (warps 2..9)
         // Warp w reads TMEM lane quadrant w % 4 (hardware restriction) and half
@@ -400,6 +513,42 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     if (lane == 0) norms[row] = acc;
 }
 
+// split-BF16 operands for the RANK mode: x_c = x - mean (fp32), hi = bf16(x_c),
+// lo = bf16(x_c - hi).  Queries get [hi | hi | lo], references [hi | lo | hi] along K, so one
+// GEMM over K' = 3 d_pad yields hi.hi + hi.lo + lo.hi (x.y to ~2^-17 relative); norms are
+// the fp32 sums of x_c^2.
+__global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
+                                  const double* __restrict__ colsum, double inv_n, int ref_layout,
+                                  __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms)
+{
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    float acc = 0.0f;
+    __nv_bfloat16* o = Xs + row * (int64_t)(3 * d_pad);
+    for (int f = lane; f < d_pad; f += 32) {
+        __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
+        if (f < d) {
+            const float c = X[row * d + f] - (float)(colsum[f] * inv_n);
+            hi = __float2bfloat16_rn(c);
+            lo = __float2bfloat16_rn(c - __bfloat162float(hi));
+            acc = fmaf(c, c, acc);
+        }
+        o[f] = hi;
+        o[d_pad + f] = ref_layout ? lo : hi;
+        o[2 * d_pad + f] = ref_layout ? hi : lo;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) norms[row] = acc;
+}
+
+// exact re-check of the ambiguous (query, reference) pairs of the RANK mode: exact R2 key,
+// bucket = first threshold it is below (R16), added to the histogram
+__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d,
+                                const int2* __restrict__ amb, const int* __restrict__ amb_count, int amb_cap,
+                                const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
+                                int64_t index_offset, int32_t* __restrict__ hist);
+
 // ----------------------------------------------------------------------------- re-rank
 // warp per query row; candidates t and t + 32 on lane t (kc <= 64); exact fp32 d2 (R2),
 // a bitonic sort of each 32-wide half by key (d2, id), then the two sorted halves are
@@ -443,6 +592,23 @@ __device__ __forceinline__ float exact_d2(const float* x, const float* y, int d)
         s = __fmaf_rn(t, t, s);
     }
     return s;
+}
+
+__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d,
+                                const int2* __restrict__ amb, const int* __restrict__ amb_count, int amb_cap,
+                                const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
+                                int64_t index_offset, int32_t* __restrict__ hist)
+{
+    const int cnt = min(amb_count[blockIdx.y], amb_cap);
+    const int2* list = amb + (int64_t)blockIdx.y * amb_cap;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
+        const int2 pr = list[e];
+        const float v = exact_d2(Xq + (int64_t)pr.x * d, Xr + (int64_t)pr.y * d, d);
+        const int32_t gid = (int32_t)(pr.y + index_offset);
+        int b = 0;
+        while (b < k && !key_less(v, gid, thr_d2[(int64_t)pr.x * k + b], thr_id[(int64_t)pr.x * k + b])) ++b;
+        if (b < k) atomicAdd(hist + (int64_t)pr.x * k + b, 1);
+    }
 }
 
 __global__ void rerank_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
@@ -545,20 +711,23 @@ umap_status prep_bf16(const float* X, int64_t n, int d, int d_pad, const double*
 
 }  // namespace
 
-template <int KC, int ST>
-size_t knn_tc_smem_bytes() { return 1024 + ST * STAGE_BYTES + 8 * (2 * ST + 4) + 16; }
+template <int KC, int ST, int MODE>
+size_t knn_tc_smem_bytes()
+{
+    return 1024 + ST * STAGE_BYTES + 8 * (2 * ST + 4) + 16 + (MODE == 1 ? 2 * TC_KT * TC_BM * 4 + 16 : 0);
+}
 
-template <int KC, int ST>
+template <int KC, int ST, int MODE = 0>
 umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
 {
-    const size_t smem = knn_tc_smem_bytes<KC, ST>();
+    const size_t smem = knn_tc_smem_bytes<KC, ST, MODE>();
     static bool configured = false;
     if (!configured) {
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
         configured = true;
     }
-    knn_tc_kernel<KC, ST><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
+    knn_tc_kernel<KC, ST, MODE><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
     UMAP_LAUNCH_CHECK("knn_tc_kernel");
     return UMAP_OK;
 }
@@ -641,5 +810,68 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     UMAP_LAUNCH_CHECK("rerank_kernel");
     return UMAP_OK;
 }
+
+
+// Input-space rank counts of trustworthiness with the tensor-core GEMM (R16): queries =
+// rows [row_begin, row_end) of X, references = all of X.  Exact thresholds in, exact
+// non-cumulative bucket counts out (hist [rows][k]); the approximate pass only decides
+// pairs whose bucket is certain under the error bound, the rest are re-checked exactly.
+// *overflow != 0 tells the caller to fall back to the exact SIMT kernel.
+umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
+                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow, cudaStream_t s)
+{
+    *overflow = 0;
+    if (rows == 0) return UMAP_OK;
+    if (k > TC_KT) { *overflow = 1; return UMAP_OK; }
+    const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
+    const int dk = 3 * d_pad;
+    Scratch colsum, xr, rn, xq, qn, amb, ambc;
+    UMAP_TRY(colsum.alloc(sizeof(double) * d, s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(colsum.p, 0, sizeof(double) * d, s));
+    {
+        dim3 grid(ceil_div(d, 32), (unsigned)std::min<int64_t>(std::max<int64_t>(1, n / 64), 512));
+        colsum_kernel<<<grid, 256, 0, s>>>(X, n, d, colsum.as<double>());
+        UMAP_LAUNCH_CHECK("colsum_kernel");
+    }
+    UMAP_TRY(xr.alloc(sizeof(__nv_bfloat16) * (size_t)n * dk, s));
+    UMAP_TRY(rn.alloc(sizeof(float) * (size_t)n, s));
+    split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n, 1,
+                                                          xr.as<__nv_bfloat16>(), rn.as<float>());
+    UMAP_LAUNCH_CHECK("split_bf16_kernel");
+    UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
+    UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
+    split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X + row_begin * (int64_t)d, rows, d, d_pad,
+                                                             colsum.as<double>(), 1.0 / (double)n, 0,
+                                                             xq.as<__nv_bfloat16>(), qn.as<float>());
+    UMAP_LAUNCH_CHECK("split_bf16_kernel");
+    CUtensorMap map_q, map_r;
+    UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
+    UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN));
+    const int64_t qblocks = (rows + TC_BM - 1) / TC_BM;
+    const int cap = TC_BM * 2048;
+    UMAP_TRY(amb.alloc(sizeof(int2) * (size_t)qblocks * cap, s));
+    UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)qblocks, s));
+    TcArgs a{};
+    a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = dk / TC_BK; a.kc = 0;
+    a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
+    a.thr_d2 = thr_d2; a.k = k; a.margin = 1e-3f; a.hist = hist; a.amb = amb.as<int2>(); a.amb_cap = cap;
+    a.amb_count = ambc.as<int>();
+    UMAP_TRY((launch_tc<32, 4, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
+    rank_fix_kernel<<<dim3(64, (unsigned)qblocks), 256, 0, s>>>(X + row_begin * (int64_t)d, X, d, amb.as<int2>(),
+                                                                 ambc.as<int>(), cap, thr_d2, thr_id, k, 0, hist);
+    UMAP_LAUNCH_CHECK("rank_fix_kernel");
+    std::vector<int> counts((size_t)qblocks);
+    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * qblocks, cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    int64_t total = 0;
+    for (int c : counts) {
+        total += c;
+        if (c > cap) *overflow = 1;
+    }
+    g_last_rank_ambiguous = total;
+    return UMAP_OK;
+}
+
+int64_t last_rank_ambiguous() { return g_last_rank_ambiguous; }
 
 }  // namespace umapb200

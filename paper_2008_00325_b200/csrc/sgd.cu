@@ -43,7 +43,13 @@ struct SgdArgs {
 __device__ __forceinline__ float clip4(float v) { return fminf(fmaxf(v, -4.0f), 4.0f); }
 
 // s^b via exp2(b log2 s); s > 0
-__device__ __forceinline__ float pow_b(float s, float b) { return exp2f(b * __log2f(s)); }
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float pow_b(float s, float b) { return ex2_approx(b * __log2f(s)); }
 
 __device__ __forceinline__ bool edge_due(float r, int e)
 {
@@ -192,21 +198,18 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, 
 
 // grid-wide barrier between epochs (cooperative launch guarantees co-residency);
 // the gpu-scope fences order the epoch's writes and invalidate L1
-__device__ __forceinline__ void grid_barrier(unsigned int* bar)
+// monotonic arrival counter: barrier number k completes when the counter reaches
+// (k + 1) * gridDim.x (no reset, one release-add and acquire polling per CTA)
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* gen = bar + 1;
-        const unsigned int my = *gen;
         __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == my) { __nanosleep(32); }
-        }
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
     }
     __syncthreads();
 }
@@ -216,12 +219,13 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar)
 // (col, r) records with coalesced loads, evaluates the closed-form schedule (R9), and
 // compacts due edges into a per-warp queue that is processed 32 at a time (every lane
 // carries a due edge during the expensive part).
-template <int DIM, bool DET, int MC, int VPW, int MINB>
+template <int DIM, bool DET, int MC, int VPW, int MINB, int CPB>
 __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(SgdArgs A)
 {
     __shared__ int32_t q_h[SGD_WARPS][QCAP];   // owner lane (0..VPW-1) of the queued edge
     __shared__ int32_t q_t[SGD_WARPS][QCAP];   // tail vertex
     __shared__ long long acc[SGD_WARPS][DIM][VPW];
+    __shared__ int s_ctr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = (int)A.n;
     const int n_chunks = (int)A.n_chunks;
@@ -231,9 +235,19 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
         const float* Yr = (DET && par) ? A.Y1 : A.Y0;
         float* Yw = DET ? (par ? A.Y0 : A.Y1) : A.Y0;
         const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
-        const int wid = blockIdx.x * SGD_WARPS + warp, nw = gridDim.x * SGD_WARPS;
-        for (int chunk = wid; chunk < (A.debug & 1 ? 0 : n_chunks); chunk += nw) {  // static round-robin (a shared
-            // work counter serialises at L2: thousands of grabs per epoch)
+        // a CTA owns CPB consecutive chunks (VPW * CPB vertices); its warps take chunks from
+        // the CTA's range through a shared-memory counter (dynamic balance inside the CTA,
+        // no global work counter: thousands of grabs per epoch would serialise at L2)
+        const int n_br = (n_chunks + CPB - 1) / CPB;
+        for (int br = blockIdx.x; br < (A.debug & 1 ? 0 : n_br); br += gridDim.x) {
+          if (threadIdx.x == 0) s_ctr = 0;
+          __syncthreads();
+          for (;;) {
+            int ci = 0;
+            if (lane == 0) ci = atomicAdd(&s_ctr, 1);
+            ci = __shfl_sync(0xffffffffu, ci, 0);
+            const int chunk = br * CPB + ci;
+            if (ci >= CPB || chunk >= n_chunks) break;
             const int v0 = chunk * VPW;
             const int nv = min(VPW, n - v0);
             // lane l < nv holds indptr[v0 + l]; the end is loaded separately (nv may be 32)
@@ -323,8 +337,10 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
                 }
             }
             __syncwarp();
+          }
+          __syncthreads();
         }
-        if (epoch + 1 < A.e_end) grid_barrier(A.bar);
+        if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1) * gridDim.x);
     }
     // due_count is warp-uniform (every lane added the same ballot counts)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
@@ -457,10 +473,10 @@ transform_sgd_kernel(const int32_t* __restrict__ idx, const float* __restrict__ 
     for (int c = 0; c < DIM; ++c) Yq[q * DIM + c] = y[c];
 }
 
-template <int DIM, bool DET, int MC, int VPW, int MINB>
+template <int DIM, bool DET, int MC, int VPW, int MINB, int CPB>
 umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
 {
-    auto kern = sgd_persistent_kernel<DIM, DET, MC, VPW, MINB>;
+    auto kern = sgd_persistent_kernel<DIM, DET, MC, VPW, MINB, CPB>;
     A.n_chunks = (A.n + VPW - 1) / VPW;
     static int max_blocks = -1;
     if (max_blocks < 0) {
@@ -468,7 +484,7 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
         UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * SGD_WARPS, 0));
         max_blocks = std::max(1, per_sm) * num_sms();
     }
-    const int64_t want = (A.n_chunks + SGD_WARPS - 1) / SGD_WARPS;
+    const int64_t want = (A.n_chunks + CPB - 1) / CPB;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, max_blocks));
     void* args[] = {&A};
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * SGD_WARPS), args, 0, s));
@@ -490,11 +506,11 @@ template <int DIM, bool DET, int MC>
 umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
 {
     switch (DIM == 2 ? sgd_variant() : 0) {
-        case 1: return launch_sgd_t<DIM, DET, MC, 16, 3>(A, s);
-        case 2: return launch_sgd_t<DIM, DET, MC, 8, 3>(A, s);
-        case 3: return launch_sgd_t<DIM, DET, MC, 32, 4>(A, s);
-        case 4: return launch_sgd_t<DIM, DET, MC, 16, 4>(A, s);
-        default: return launch_sgd_t<DIM, DET, MC, 32, 3>(A, s);
+        case 1: return launch_sgd_t<DIM, DET, MC, 32, 3, 8>(A, s);
+        case 2: return launch_sgd_t<DIM, DET, MC, 8, 3, 32>(A, s);
+        case 3: return launch_sgd_t<DIM, DET, MC, 16, 3, 32>(A, s);
+        case 4: return launch_sgd_t<DIM, DET, MC, 32, 3, 16>(A, s);
+        default: return launch_sgd_t<DIM, DET, MC, 16, 3, 16>(A, s);
     }
 }
 
@@ -575,7 +591,7 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
     }
     UMAP_TRY(counter.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), s));
-    const size_t bar_words = 2 + (size_t)(e_end - e_begin);
+    const size_t bar_words = 2;
     UMAP_TRY(bar.alloc(bar_words * sizeof(unsigned int), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(bar.p, 0, bar_words * sizeof(unsigned int), s));
     const bool det = p->sgd_mode == UMAP_SGD_DETERMINISTIC;

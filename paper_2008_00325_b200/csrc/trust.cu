@@ -14,6 +14,9 @@ umap_status rank_count_exact(const float* Xq, int64_t nq, const float* X, int64_
                              int64_t self_offset, const float* thr_d2, const int32_t* thr_id, int32_t* cnt_out,
                              Scratch& tmp, int* n_splits_out, cudaStream_t s);
 
+umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
+                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow, cudaStream_t s);
+
 namespace {
 
 // thresholds: key (d2_X(i, j_t), j_t) for the k embedding neighbours of row i, sorted by key.
@@ -64,7 +67,7 @@ __global__ void penalty_kernel(const int32_t* __restrict__ cnt, int n_splits, in
 }  // namespace
 
 umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
-                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, cudaStream_t s)
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, cudaStream_t s)
 {
     const int64_t rows = row_end - row_begin;
     if (rows <= 0) { if (penalty_host) *penalty_host = 0; return UMAP_OK; }
@@ -78,8 +81,13 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
                                                           thr_i.as<int32_t>());
     UMAP_LAUNCH_CHECK("thresholds_kernel");
     int n_splits = 1;
-    UMAP_TRY(rank_count_exact(X + row_begin * (int64_t)d, rows, X, n, d, k, row_begin, thr_d.as<float>(),
-                              thr_i.as<int32_t>(), cnt.as<int32_t>(), tmp, &n_splits, s));
+    int overflow = 1;
+    if (knn_mode == UMAP_KNN_TENSOR_BF16)
+        UMAP_TRY(rank_count_tc(X, n, d, row_begin, rows, k, thr_d.as<float>(), thr_i.as<int32_t>(), cnt.as<int32_t>(),
+                               &overflow, s));
+    if (overflow)  // exact mode, or the tensor pass could not certify enough pairs
+        UMAP_TRY(rank_count_exact(X + row_begin * (int64_t)d, rows, X, n, d, k, row_begin, thr_d.as<float>(),
+                                  thr_i.as<int32_t>(), cnt.as<int32_t>(), tmp, &n_splits, s));
     const int32_t* counts = n_splits == 1 ? cnt.as<int32_t>() : tmp.as<int32_t>();
     penalty_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(counts, n_splits, rows, k, row_pen,
                                                        total.as<unsigned long long>());

@@ -66,11 +66,13 @@ def sharded_knn(X, k, group=None, knn_fn=None, merge_fn=None):
     return merge_fn(torch.stack(gi), torch.stack(gd), k)
 
 
-def sharded_trust_penalty(X, emb_idx, k, group=None, penalty_fn=None):
+def sharded_trust_penalty(X, emb_idx, k, group=None, penalty_fn=None, knn_mode="exact"):
     """Integer trust penalty S with rows sharded; one all-reduce.  emb_idx: n x k embedding kNN."""
     if penalty_fn is None:
         from . import api
-        penalty_fn = api.trust_penalty
+
+        def penalty_fn(X, e, k, lo, hi):
+            return api.trust_penalty(X, e, k, lo, hi, knn_mode=knn_mode)
     rank, world = _rank_world(group)
     n = X.shape[0]
     lo, hi = shard_range(n, rank, world)
@@ -82,11 +84,11 @@ def sharded_trust_penalty(X, emb_idx, k, group=None, penalty_fn=None):
     return int(t.item())
 
 
-def sharded_trustworthiness(X, Y, k, group=None, knn_fn=None, penalty_fn=None):
+def sharded_trustworthiness(X, Y, k, group=None, knn_fn=None, penalty_fn=None, knn_mode="exact"):
     """T(k) with the input-space rank counts sharded by rows (R16)."""
     knn_fn = knn_fn or _default_knn()
     emb_idx, _ = knn_fn(Y, Y, k, exclude_self=True)
-    S = sharded_trust_penalty(X, emb_idx, k, group=group, penalty_fn=penalty_fn)
+    S = sharded_trust_penalty(X, emb_idx, k, group=group, penalty_fn=penalty_fn, knn_mode=knn_mode)
     n = X.shape[0]
     return 1.0 - (2.0 / (n * k * (2.0 * n - 3.0 * k - 1.0))) * S, S
 

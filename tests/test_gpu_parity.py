@@ -369,6 +369,25 @@ def test_trust_penalty_exact(O, n, d, k):
     assert np.array_equal(np_(pen), pen_ref[100:250])
 
 
+# tensor-core rank counting (split-BF16 GEMM + certified buckets + exact re-check): the
+# integer penalty must equal the oracle's exactly
+@pytest.mark.parametrize("n,d,k,kind,emb", [(1500, 64, 15, "lowrank", "random"), (1200, 784, 15, "lowrank", "proj"),
+                                            (900, 100, 5, "iso", "random"), (700, 3, 15, "ties", "proj"),
+                                            (2000, 50, 16, "lowrank", "proj"), (333, 3072, 5, "lowrank", "random")])
+def test_trust_tensor_exact_penalty(O, n, d, k, kind, emb):
+    X = _data(kind, n, d, seed=13)
+    if emb == "random":
+        Y = synth.uniform_embedding(n, 2, seed=3)
+    else:
+        Y = (X[:, :2] + np.random.default_rng(0).standard_normal((n, 2)) * 0.5).astype(np.float32)
+    S_ref, pen_ref = O.trust_penalty(X, Y, k)
+    T, S = U.trustworthiness(cu(X), cu(Y), k, knn_mode="tensor")
+    assert S == S_ref
+    emb_idx, _ = O.knn(Y, Y, k, self_offset=0)
+    S2, pen = U.trust_penalty(cu(X), cu(emb_idx[17:300]), k, 17, 300, knn_mode="tensor")
+    assert np.array_equal(np_(pen), pen_ref[17:300])
+
+
 def test_trust_identity_is_one():
     X = cu(synth.lowrank(500, 6))
     T, S = U.trustworthiness(X, X, 10)

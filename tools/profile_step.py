@@ -17,4 +17,4 @@ X = torch.from_numpy(synth.lowrank(c["n"], c["d"], c["blobs"], c["seed"])).cuda(
 Y, st = U.fit(X, n_neighbors=c["k"], n_epochs=a.epochs or c["n_epochs"], knn_mode=a.knn_mode, sgd_mode=a.sgd_mode)
 print(st)
 if not a.no_trust:
-    print(U.trustworthiness(X, Y, 15))
+    print(U.trustworthiness(X, Y, 15, knn_mode=a.knn_mode))
