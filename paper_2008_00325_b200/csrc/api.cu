@@ -17,6 +17,7 @@ umap_status knn_exact(const float* Xq, int64_t nq, const float* Xr, int64_t nr, 
 umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
                        int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
                        float* dist, cudaStream_t s);
+umap_status knn_grid2d(const float* Y, int64_t n, int k, int out_squared, int32_t* idx, float* dist, cudaStream_t s);
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
                        int out_squared, int32_t* idx, float* dist, cudaStream_t s);
 umap_status smooth_knn(const float* dist, const int32_t* idx, int64_t n, int k, float* rho, float* sigma, float* w,
@@ -210,6 +211,9 @@ umap_status run_knn(const umap_params* p, const float* Xq, int64_t nq, const flo
                     int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
                     float* dist, cudaStream_t s)
 {
+    // 2-D self-kNN (the embedding side of trustworthiness): exact uniform-grid search
+    if (d == 2 && Xq == Xr && nq == nr && exclude_self && self_shift == 0 && index_offset == 0 && k <= 32)
+        return knn_grid2d(Xq, nq, k, out_squared, idx, dist, s);
     if (p->knn_mode == UMAP_KNN_TENSOR_BF16)
         return knn_tensor(Xq, nq, Xr, nr, d, k, std::min(64, std::max(k, p->knn_candidates)), self_shift,
                           exclude_self, index_offset, out_squared, idx, dist, s);
@@ -667,7 +671,11 @@ umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int3
     Scratch eidx, edist;
     UMAP_TRY(eidx.alloc(sizeof(int32_t) * (size_t)n * k, s));
     UMAP_TRY(edist.alloc(sizeof(float) * (size_t)n * k, s));
-    UMAP_TRY(knn_exact(Yd.p, n, Yd.p, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
+    {
+        umap_params pe;
+        umap_params_default(&pe);
+        UMAP_TRY(run_knn(&pe, Yd.p, n, Yd.p, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
+    }
     int64_t S = 0;
     UMAP_TRY(trust_penalty(Xd.p, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, s));
     const double nn = (double)n, kk = (double)k;

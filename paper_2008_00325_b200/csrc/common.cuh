@@ -102,6 +102,50 @@ template <class T> __device__ __forceinline__ T warp_sum(T v)
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
+
+// R2 exact distance: sequential fmaf in ascending feature order (float4 loads when the
+// rows are 16-byte aligned; the accumulation order is unchanged).
+__device__ __forceinline__ float exact_d2(const float* x, const float* y, int d)
+{
+    float s = 0.0f;
+    int f = 0;
+    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        const float4* y4 = reinterpret_cast<const float4*>(y);
+        for (; f + 4 <= d; f += 4) {
+            const float4 a = __ldg(x4 + (f >> 2)), b = __ldg(y4 + (f >> 2));
+            float t = __fsub_rn(a.x, b.x); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.y, b.y); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.z, b.z); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.w, b.w); s = __fmaf_rn(t, t, s);
+        }
+    }
+    for (; f < d; ++f) {
+        const float t = __fsub_rn(__ldg(x + f), __ldg(y + f));
+        s = __fmaf_rn(t, t, s);
+    }
+    return s;
+}
+
+// ascending bitonic sort of 32 (key, id) pairs across a warp (lane i ends with rank i)
+__device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)
+{
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const float ok = __shfl_xor_sync(0xffffffffu, key, stride);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
+            const bool up = ((lane & size) == 0);
+            const bool lower = (lane & stride) == 0;
+            const bool other_less = key_less(ok, oi, key, id);
+            const bool take = lower ? (up ? other_less : !other_less) : (up ? !other_less : other_less);
+            if (take && !(ok == key && oi == id)) { key = ok; id = oi; }
+        }
+    }
+}
+
+
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 }  // namespace umapb200

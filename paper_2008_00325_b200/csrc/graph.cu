@@ -271,6 +271,10 @@ umap_status exclusive_scan(const Tin* in, int64_t n, int64_t* out, cudaStream_t 
     return UMAP_OK;
 }
 template umap_status exclusive_scan<int32_t>(const int32_t*, int64_t, int64_t*, cudaStream_t);
+umap_status exclusive_scan_i32(const int32_t* in, int64_t n, int64_t* out, cudaStream_t s)
+{
+    return exclusive_scan<int32_t>(in, n, out, s);
+}
 template umap_status exclusive_scan<int64_t>(const int64_t*, int64_t, int64_t*, cudaStream_t);
 
 umap_status fuzzy_union(const int32_t* acol, const float* aw, int64_t n, int k, int64_t* indptr, int32_t* col,

@@ -154,9 +154,9 @@ struct TcArgs {
     int k;
     float margin;           // c: |d2~ - d2_exact| < c (|q|^2 + |r|^2)
     int32_t* hist;          // [n_q][k] certain bucket counts (written, not accumulated)
-    int2* amb;              // per-CTA regions of (query row, reference row) pairs to re-check
-    int amb_cap;            // capacity per CTA region
-    int* amb_count;         // [gridDim.x] entries used per CTA (may exceed cap -> overflow)
+    int32_t* amb;           // per (query row, column half) lists of reference rows to re-check
+    int amb_cap;            // capacity per list
+    int* amb_count;         // [n_q][2] entries per list (may exceed cap -> overflow)
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
@@ -273,12 +273,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const float c_m = a.margin;
         // shared histogram [half][t][row] after the ring region (ring stays untouched)
         int32_t* Hs = reinterpret_cast<int32_t*>(stage_base + TC_STAGES * STAGE_BYTES + 8 * (2 * TC_STAGES + 4) + 16);
-        int* s_amb = reinterpret_cast<int*>(Hs + 2 * TC_KT * TC_BM);
 #pragma unroll
         for (int t = 0; t < TC_KT; ++t) Hs[(half * TC_KT + t) * TC_BM + row] = 0;
-        if (warp == 2 && lane == 0) *s_amb = 0;
         asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
-        int2* amb_base = a.amb + (int64_t)blockIdx.x * a.amb_cap;
+        int32_t* amb_row = a.amb + (valid ? (q * 2 + half) * (int64_t)a.amb_cap : 0);
+        int n_amb = 0;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
@@ -326,15 +325,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     }
                     const bool amb = has && b_hi != b_lo;
                     if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
-                    const unsigned am = __ballot_sync(0xffffffffu, amb);
-                    if (am) {
-                        int base = 0;
-                        if (lane == 0) base = atomicAdd(s_amb, __popc(am));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (amb) {
-                            const int pos = base + __popc(am & ((1u << lane) - 1u));
-                            if (pos < a.amb_cap) amb_base[pos] = make_int2((int)q, (int)(jb + u));
-                        }
+                    if (amb) {
+                        if (n_amb < a.amb_cap) amb_row[n_amb] = (int32_t)(jb + u);
+                        ++n_amb;
                     }
                 }
             }
@@ -347,7 +340,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             for (int t = 0; t < k; ++t)
                 a.hist[q * k + t] = Hs[t * TC_BM + row] + Hs[(TC_KT + t) * TC_BM + row];
         }
-        if (warp == 2 && lane == 0) a.amb_count[blockIdx.x] = *s_amb;
+        if (valid) a.amb_count[q * 2 + half] = n_amb;
     } else {
         // ---------------------------------------------------- epilogue (warps 2..9)
         // Warp w reads TMEM lane quadrant w % 4 (hardware restriction) and half
@@ -542,73 +535,48 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
     if (lane == 0) norms[row] = acc;
 }
 
-// exact re-check of the ambiguous (query, reference) pairs of the RANK mode: exact R2 key,
-// bucket = first threshold it is below (R16), added to the histogram
-__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d,
-                                const int2* __restrict__ amb, const int* __restrict__ amb_count, int amb_cap,
-                                const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
-                                int64_t index_offset, int32_t* __restrict__ hist);
-
 // ----------------------------------------------------------------------------- re-rank
 // warp per query row; candidates t and t + 32 on lane t (kc <= 64); exact fp32 d2 (R2),
 // a bitonic sort of each 32-wide half by key (d2, id), then the two sorted halves are
 // merged by rank (keys are distinct: ids differ) and the first k written.
-__device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)
-{
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const float ok = __shfl_xor_sync(0xffffffffu, key, stride);
-            const int32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
-            const bool up = ((lane & size) == 0);
-            const bool lower = (lane & stride) == 0;
-            const bool other_less = key_less(ok, oi, key, id);
-            const bool take = lower ? (up ? other_less : !other_less) : (up ? !other_less : other_less);
-            if (take && !(ok == key && oi == id)) { key = ok; id = oi; }
-        }
-    }
-}
-
-// R2 exact distance: sequential fmaf in ascending feature order (float4 loads when the
-// rows are 16-byte aligned; the accumulation order is unchanged).
-__device__ __forceinline__ float exact_d2(const float* x, const float* y, int d)
-{
-    float s = 0.0f;
-    int f = 0;
-    if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0) {
-        const float4* x4 = reinterpret_cast<const float4*>(x);
-        const float4* y4 = reinterpret_cast<const float4*>(y);
-        for (; f + 4 <= d; f += 4) {
-            const float4 a = __ldg(x4 + (f >> 2)), b = __ldg(y4 + (f >> 2));
-            float t = __fsub_rn(a.x, b.x); s = __fmaf_rn(t, t, s);
-            t = __fsub_rn(a.y, b.y); s = __fmaf_rn(t, t, s);
-            t = __fsub_rn(a.z, b.z); s = __fmaf_rn(t, t, s);
-            t = __fsub_rn(a.w, b.w); s = __fmaf_rn(t, t, s);
-        }
-    }
-    for (; f < d; ++f) {
-        const float t = __fsub_rn(__ldg(x + f), __ldg(y + f));
-        s = __fmaf_rn(t, t, s);
-    }
-    return s;
-}
-
-__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d,
-                                const int2* __restrict__ amb, const int* __restrict__ amb_count, int amb_cap,
+// Exact re-check of the RANK mode's ambiguous pairs (R16).  Warp per query row: the
+// row's two lists (one per column half) hold reference ids; each lane takes pairs,
+// computes the exact R2 key and its bucket (first threshold it is below), the warp
+// accumulates a shared histogram and adds it to the row's certain counts.
+__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
+                                const int32_t* __restrict__ amb, const int* __restrict__ amb_count, int cap_row,
                                 const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
                                 int64_t index_offset, int32_t* __restrict__ hist)
 {
-    const int cnt = min(amb_count[blockIdx.y], amb_cap);
-    const int2* list = amb + (int64_t)blockIdx.y * amb_cap;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        const int2 pr = list[e];
-        const float v = exact_d2(Xq + (int64_t)pr.x * d, Xr + (int64_t)pr.y * d, d);
-        const int32_t gid = (int32_t)(pr.y + index_offset);
-        int b = 0;
-        while (b < k && !key_less(v, gid, thr_d2[(int64_t)pr.x * k + b], thr_id[(int64_t)pr.x * k + b])) ++b;
-        if (b < k) atomicAdd(hist + (int64_t)pr.x * k + b, 1);
+    __shared__ int h[8][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * 8 + warp;
+    if (q >= nq) return;
+    if (lane < 16) h[warp][lane] = 0;
+    __syncwarp();
+    const float* x = Xq + q * (int64_t)d;
+    float td[16];
+    int32_t ti[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        td[t] = t < k ? thr_d2[q * k + t] : INFINITY;
+        ti[t] = t < k ? thr_id[q * k + t] : INT32_MAX;
     }
+    for (int hf = 0; hf < 2; ++hf) {
+        const int cnt = min(amb_count[q * 2 + hf], cap_row);
+        const int32_t* list = amb + (q * 2 + hf) * (int64_t)cap_row;
+        for (int e = lane; e < cnt; e += 32) {
+            const int32_t l = list[e];
+            const float v = exact_d2(x, Xr + (int64_t)l * d, d);
+            const int32_t gid = (int32_t)(l + index_offset);
+            int b = 0;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) b += (t < k) && !key_less(v, gid, td[t], ti[t]);
+            if (b < k) atomicAdd(&h[warp][b], 1);
+        }
+    }
+    __syncwarp();
+    if (lane < k) hist[q * k + lane] += h[warp][lane];
 }
 
 __global__ void rerank_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
@@ -848,20 +816,20 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
     UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN));
     const int64_t qblocks = (rows + TC_BM - 1) / TC_BM;
-    const int cap = TC_BM * 2048;
-    UMAP_TRY(amb.alloc(sizeof(int2) * (size_t)qblocks * cap, s));
-    UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)qblocks, s));
+    const int cap = 2048;
+    UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * 2 * cap, s));
+    UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * 2, s));
     TcArgs a{};
     a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = dk / TC_BK; a.kc = 0;
     a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
-    a.thr_d2 = thr_d2; a.k = k; a.margin = 1e-3f; a.hist = hist; a.amb = amb.as<int2>(); a.amb_cap = cap;
+    a.thr_d2 = thr_d2; a.k = k; a.margin = 5e-4f; a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     a.amb_count = ambc.as<int>();
     UMAP_TRY((launch_tc<32, 4, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
-    rank_fix_kernel<<<dim3(64, (unsigned)qblocks), 256, 0, s>>>(X + row_begin * (int64_t)d, X, d, amb.as<int2>(),
-                                                                 ambc.as<int>(), cap, thr_d2, thr_id, k, 0, hist);
+    rank_fix_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),
+                                                      ambc.as<int>(), cap, thr_d2, thr_id, k, 0, hist);
     UMAP_LAUNCH_CHECK("rank_fix_kernel");
-    std::vector<int> counts((size_t)qblocks);
-    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * qblocks, cudaMemcpyDeviceToHost, s));
+    std::vector<int> counts((size_t)rows * 2);
+    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * 2, cudaMemcpyDeviceToHost, s));
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
     int64_t total = 0;
     for (int c : counts) {

@@ -45,6 +45,27 @@ __global__ void thresholds_kernel(const float* __restrict__ X, int d, const int3
     }
 }
 
+// k <= 32: warp per row, lane t computes the exact key of threshold t, warp bitonic sort
+__global__ void thresholds_warp_kernel(const float* __restrict__ X, int d, const int32_t* __restrict__ emb_idx,
+                                       int64_t rows, int64_t row_begin, int k, float* __restrict__ thr_d2,
+                                       int32_t* __restrict__ thr_id)
+{
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    float key = INFINITY;
+    int32_t id = INT32_MAX;
+    if (lane < k) {
+        id = emb_idx[r * k + lane];
+        key = exact_d2(X + (row_begin + r) * (int64_t)d, X + (int64_t)id * d, d);
+    }
+    warp_bitonic(key, id, lane);
+    if (lane < k) {
+        thr_d2[r * k + lane] = key;
+        thr_id[r * k + lane] = id;
+    }
+}
+
 // penalty of row r: counts (summed over reference splits) -> cumulative -> ranks.
 __global__ void penalty_kernel(const int32_t* __restrict__ cnt, int n_splits, int64_t rows, int k,
                                int64_t* __restrict__ row_pen, unsigned long long* __restrict__ total)
@@ -77,9 +98,15 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
     UMAP_TRY(cnt.alloc(sizeof(int32_t) * (size_t)rows * k, s));
     UMAP_TRY(total.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(total.p, 0, sizeof(unsigned long long), s));
-    thresholds_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(),
-                                                          thr_i.as<int32_t>());
-    UMAP_LAUNCH_CHECK("thresholds_kernel");
+    if (k <= 32) {
+        thresholds_warp_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X, d, emb_idx, rows, row_begin, k,
+                                                                        thr_d.as<float>(), thr_i.as<int32_t>());
+        UMAP_LAUNCH_CHECK("thresholds_warp_kernel");
+    } else {
+        thresholds_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(),
+                                                              thr_i.as<int32_t>());
+        UMAP_LAUNCH_CHECK("thresholds_kernel");
+    }
     int n_splits = 1;
     int overflow = 1;
     if (knn_mode == UMAP_KNN_TENSOR_BF16)

@@ -52,6 +52,10 @@ KNN_CASES = [
     (600, 3, 15, "ties"),
     (129, 17, 15, "ties"),
     (20, 5, 19, "lowrank"),
+    (5000, 2, 15, "lowrank"),   # 2-D: exact uniform-grid path
+    (3000, 2, 32, "iso"),
+    (1000, 2, 15, "ties"),
+    (40, 2, 7, "ties"),
 ]
 
 
