@@ -216,6 +216,9 @@ UMAP_API const char* umap_status_string(umap_status s);
 UMAP_API const char* umap_last_error(void);
 /* Number of this library's kernels launched by the calling thread since load. */
 UMAP_API int64_t     umap_kernel_launch_count(void);
+/* Diagnostics: pairs the calling thread's last tensor-mode trustworthiness call could not
+ * certify from the tensor-core pass and re-checked exactly. */
+UMAP_API int64_t     umap_trust_ambiguous_count(void);
 /* Library version string. */
 UMAP_API const char* umap_version(void);
 

@@ -71,6 +71,7 @@ SIGNATURES = {
     "umap_last_error": (ctypes.c_char_p, []),
     "umap_kernel_launch_count": (c_int64, []),
     "umap_version": (ctypes.c_char_p, []),
+    "umap_trust_ambiguous_count": (c_int64, []),
 }
 
 _lib = None

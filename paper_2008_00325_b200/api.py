@@ -241,5 +241,10 @@ def kernel_launch_count():
     return int(_lib.load().umap_kernel_launch_count())
 
 
+def trust_ambiguous_count():
+    """pairs the last tensor-mode trust call re-checked exactly (diagnostic)."""
+    return int(_lib.load().umap_trust_ambiguous_count())
+
+
 def version():
     return _lib.load().umap_version().decode()

@@ -34,6 +34,7 @@ umap_status transform_optimize(const int32_t* idx, const float* w, int64_t nq, i
 umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
                           int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, cudaStream_t s);
 bool dim_supported(int dim);
+int64_t last_rank_ambiguous();
 
 // ---- error state
 static thread_local std::string g_last_error;
@@ -230,6 +231,8 @@ extern "C" {
 const char* umap_version(void) { return "umap-b200 0.1 (sm_100a)"; }
 
 int64_t umap_kernel_launch_count(void) { return g_launches; }
+
+int64_t umap_trust_ambiguous_count(void) { return last_rank_ambiguous(); }
 
 const char* umap_last_error(void) { return g_last_error.c_str(); }
 

@@ -28,7 +28,7 @@
 
 namespace umapb200 {
 
-static int64_t g_last_rank_ambiguous = 0;
+static thread_local int64_t g_last_rank_ambiguous = 0;
 
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
                        int out_squared, int32_t* idx, float* dist, cudaStream_t s);
@@ -822,7 +822,9 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     TcArgs a{};
     a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = dk / TC_BK; a.kc = 0;
     a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
-    a.thr_d2 = thr_d2; a.k = k; a.margin = 5e-4f; a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
+    a.thr_d2 = thr_d2; a.k = k; a.margin = 5e-4f;
+    if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
+    a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     a.amb_count = ambc.as<int>();
     UMAP_TRY((launch_tc<32, 4, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     rank_fix_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One GPU call: parity tests, smoke, bench, launch list + ncu --set full of the top kernels.
+# usage (on the GPU box): bash tools/gpu_full.sh <tag>
+TAG=${1:-r01}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_${TAG}.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/pytest_gpu_${TAG}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+timeout 600 python bench.py --sgd-mode hogwild --no-cpu-baseline --no-e2e > gpurun_out/bench_hog_${TAG}.json 2>> gpurun_out/bench_${TAG}.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_${TAG}.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'knn_tc|sgd_persistent|rerank|rank_fix|grid_knn|thresholds|smooth_knn|union_rows' \
+    -c 10 -o gpurun_out/prof_${TAG} -f python tools/profile_step.py --knn-mode tensor > gpurun_out/prof_${TAG}.log 2>&1
+ls -la gpurun_out
+tail -3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log
+cat gpurun_out/bench_${TAG}.json gpurun_out/bench_hog_${TAG}.json

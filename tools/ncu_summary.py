@@ -1,0 +1,41 @@
+"""Summarise an ncu --set full report into profiles/: per kernel duration, DRAM bytes,
+L2 sectors, SM / tensor / DRAM throughput.  usage: python tools/ncu_summary.py <rep> <out.json> [<launches.csv>]"""
+import csv, io, json, subprocess, sys
+
+M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
+     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+     "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+     "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed",
+     "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+     "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+     "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+     "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct"]
+rep, out = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h = rows[0]
+res = {"source": rep, "kernels": {}}
+for r in rows[2:]:
+    d = dict(zip(h, r))
+    name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("umapb200::", "").replace("<unnamed>::", "")
+    rec = {}
+    for m in M:
+        if m in d:
+            try:
+                rec[m] = float(d[m].replace(",", ""))
+            except ValueError:
+                rec[m] = d[m]
+    if "dram__bytes_read.sum" in rec:
+        rec["dram_bytes_per_launch"] = rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
+    key = name
+    i = 2
+    while key in res["kernels"]:
+        key = f"{name}#{i}"; i += 1
+    res["kernels"][key] = rec
+json.dump(res, open(out, "w"), indent=1)
+for k, v in res["kernels"].items():
+    print(f"{k[:48]:48s} {v.get('gpu__time_duration.sum', 0) / 1e6:9.3f} ms  dram {v.get('dram_bytes_per_launch', 0) / 1e6:9.1f} MB"
+          f"  L2 {v.get('lts__t_sectors.sum', 0) * 32 / 1e9:7.2f} GB  sm {v.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):5.1f}%"
+          f"  tensor {v.get('sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed', '-')}")
