@@ -4,9 +4,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config C2] [--knn-mode exact|tensor] [--sgd-mode deterministic|hogwild]
 
-A step = one pass of the whole hot path over the config's synthetic input: umap_fit
-(a1 validate, a2 kNN, a3/a4 rho-sigma-membership, a5 fuzzy union, a6/a7 schedule +
-init, a8 SGD epochs) followed by umap_trustworthiness (a10) of the result.
+A step = one pass of the whole hot path over the config's synthetic input: one umap_fit
+call with trust_k = 15 (a1 validate, a2 kNN, a3/a4 rho-sigma-membership, a5 fuzzy union,
+a6/a7 schedule + init, a8 SGD epochs, a10 trustworthiness of the result).
 N = 1: configs[1] (C2, MNIST-shaped 70,000 x 784, k=15, 2-D, 500 epochs).
 N > 1: the kNN index rows and the trust rows are sharded across ranks (NCCL
 all-gather / all-reduce), graph + SGD replicated (strong scaling, dist.py).
@@ -33,7 +33,7 @@ METRIC = "fit wall-s & SGD edge-updates/s at MNIST-70k shape; trustworthiness"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -46,7 +46,8 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampled every 50 ms (B200_PROFILING.md clocks line); only samples that arrive
+    between mark_begin() and mark_end() (the timed region) are summarised."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -54,11 +55,12 @@ class ClockSampler:
         self.index = index
         self.samples = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -69,19 +71,29 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.samples.append(parts)
+                self.samples.append((time.perf_counter(), parts))
+
+    def mark_begin(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        win = [p for t, p in self.samples if t0 <= t <= t1 + 0.05]
         sm, smax, reasons = [], None, set()
-        for s in self.samples:
+        for s in win:
             try:
                 sm.append(float(s[0]))
                 smax = float(s[1])
@@ -90,9 +102,8 @@ class ClockSampler:
             for nm, v in zip(names, s[2:]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        load = [x for x in sm if smax and x > 0.3 * smax] or sm
-        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(win), "window": "timed region"}
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -100,26 +111,61 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p, "measured"
+        return p, "measured (MEASURED_PEAKS.json)"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, \
-            "fallback"
+            "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic(name):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+# library profile slot -> kernel name in the ncu summaries (profiles/ncu_*.json)
+NCU_NAME = {"knn_tc_kernel (kNN candidates)": "knn_tc_kernel<32, 4, 0>",
+            "knn_tc_kernel (trust ranks)": "knn_tc_kernel<32, 4, 1>",
+            "sgd_persistent_kernel": "sgd_persistent_kernel", "rank_fix_kernel": "rank_fix_kernel",
+            "rerank_kernel": "rerank_kernel", "thresholds_warp_kernel": "thresholds_warp_kernel",
+            "grid_knn_kernel": "grid_knn_kernel", "smooth_knn_kernel": "smooth_knn_kernel"}
+
+
+def profile_traffic(slot):
+    """DRAM bytes (read + write) per launch of a kernel from the newest committed ncu --set full
+    summary, or None."""
+    import glob
+    want = NCU_NAME.get(slot)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*.json")), key=os.path.getmtime)
+    if not want or not files:
+        return None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+        with open(files[-1]) as f:
             d = json.load(f)
-        return d.get("kernels", {}).get(name, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
-        return None
+        return None, None
+    for name, rec in d.get("kernels", {}).items():
+        if want in name and "dram_bytes_per_launch" in rec:
+            return rec["dram_bytes_per_launch"], os.path.relpath(files[-1], ROOT)
+    return None, None
 
 
 def cfg_of(name):
     import synth
     c = dict(synth.CONFIGS[name])
     return c
+
+
+def kernel_work(slot, c, st, n_amb):
+    """Algorithmic work of one step of a kernel: (bound, amount, unit)."""
+    n, d, k, N, m, dim = c["n"], c["d"], c["k"], c["n_epochs"], 5, 2
+    if slot.startswith("knn_tc_kernel"):
+        return "tensor", 2.0 * n * n * d, "flop"          # the n x n x d distance contraction, unpadded
+    if slot == "sgd_persistent_kernel":                    # SURVEY 8(d) byte model
+        return "hbm", 8.0 * st["nnz"] * (N - 1) + 4.0 * dim * (m + 1) * st["positives"] + 8.0 * dim * n * (N - 1), "B"
+    if slot == "rank_fix_kernel":
+        return "hbm", 4.0 * d * n_amb, "B"                 # one fp32 reference row per re-checked pair
+    if slot == "rerank_kernel":
+        return "hbm", 4.0 * d * n * max(32, 2 * k), "B"   # k' candidate rows per query
+    if slot == "thresholds_warp_kernel":
+        return "hbm", 4.0 * d * n * 15, "B"                # one row per embedding neighbour
+    if slot == "smooth_knn_kernel":
+        return "hbm", 16.0 * n * k, "B"                    # dist + idx in, w + col out
+    return None, None, None
 
 
 # ----------------------------------------------------------------------------- cpu oracle timing
@@ -218,12 +264,12 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
 
     def step(Xd):
+        """one pass of a1..a10: umap_fit with the trustworthiness of its result (trust_k)"""
         if world == 1:
-            Y, st = U.fit(Xd, **kw)
-            T, S = U.trustworthiness(Xd, Y, trust_k, knn_mode=args.knn_mode)
-        else:
-            Y, st = D.sharded_fit(Xd, **kw)
-            T, S = D.sharded_trustworthiness(Xd, Y, trust_k, knn_mode=args.knn_mode)
+            Y, st = U.fit(Xd, trust_k=trust_k, **kw)
+            return Y, st, st["trustworthiness"]
+        Y, st = D.sharded_fit(Xd, **kw)
+        T, S = D.sharded_trustworthiness(Xd, Y, trust_k, knn_mode=args.knn_mode)
         return Y, st, T
 
     def barrier():
@@ -231,16 +277,18 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         step(X)
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    clocks.start()
     launches0 = U.kernel_launch_count()
     stats = []
     T = None
     barrier()
+    clocks.mark_begin()
+    U.profile_begin()  # per-kernel CUDA events on the launching stream, inside the timed region
     for i in range(args.steps):
         flush.fill_(float(i))  # L2 flush between timed steps (untimed)
         ev[i][0].record()
@@ -248,8 +296,10 @@ def run_ours(args):
         ev[i][1].record()
         stats.append(st)
     barrier()
+    prof = U.profile_end()
+    clocks.mark_end()
     launches = U.kernel_launch_count() - launches0
-    clk = clocks.stop()
+    n_amb = U.trust_ambiguous_count()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     ms = sum(ms_steps) / len(ms_steps)
     if world > 1:
@@ -257,30 +307,23 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    # ---- e2e through the public API with host buffers: H2D of X, fit, trust, D2H of Y and T
+    # ---- e2e through the public C ABI with HOST buffers: umap_fit(X host -> Y host, trust_k):
+    # the library stages X host->device and Y device->host inside the call
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         e2e_ms = []
+        Y_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
         for i in range(max(1, min(args.steps, 3))):
             flush.fill_(float(i))
             barrier()
             t0 = time.perf_counter()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            Xd = X_host.to("cuda", non_blocking=True)
-            Y, st, Te = step(Xd)
-            Yh = Y.to("cpu")
-            e1.record()
-            torch.cuda.synchronize()
-            e2e_ms.append(e0.elapsed_time(e1))
-            del Xd
+            _, st_e = U.fit(X_host, out=Y_host, trust_k=trust_k, **kw)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
         em = sum(e2e_ms) / len(e2e_ms)
-        if world > 1:
-            t = torch.tensor([em], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            em = float(t.item())
         e2e = {"value": em / 1e3, "unit": "s", "h2d_bytes_per_step": int(X_host.numel() * 4),
-               "d2h_bytes_per_step": int(Yh.numel() * 4 + 8)}
+               "d2h_bytes_per_step": int(Y_host.numel() * 4 + 8 + 8), "api": "umap_fit(X host, Y host, trust_k=15)",
+               "timer": "host wall clock around the synchronous call"}
+    clk = clocks.stop()
 
     if rank != 0:
         if world > 1:
@@ -292,57 +335,78 @@ def run_ours(args):
     pk, pk_kind = peaks()
     positives = st["positives"]
     sgd_s = st["ms_sgd"] / 1e3
-    # dominant kernel: the distance-tile kernel of the kNN stage (exact mode: fp32 SIMT ALU-bound)
-    if args.knn_mode == "exact":
-        # 2 fp32 lane-instructions (FADD + FFMA) per (query, reference, feature); peak = 148 SMs x
-        # 128 FP32 lanes x sm_max clock
-        work = 2.0 * n * n * d
-        sm_hz = (pk.get("sm_max_mhz") or 1965.0) * 1e6
-        peak = 148 * 128 * sm_hz / 1e12
-        achieved = work / (st["ms_knn"] / 1e3) / 1e12
-        roof = {"kernel": "dist_tile_kernel<16,0> (kNN, exact fp32)", "bound": "alu", "achieved": achieved,
-                "peak": peak, "unit": "Tinst/s (fp32 FADD+FFMA lane-ops)", "frac": achieved / peak,
-                "traffic": profile_traffic("dist_tile_kernel"), "peak_source": "derived: 148 SM x 128 lanes x sm_max",
-                "duration_ms": st["ms_knn"]}
-    else:
-        flops = 2.0 * n * n * d
-        peak = pk.get("bf16_tflops", 1590.0)
-        achieved = flops / (st["ms_knn"] / 1e3) / 1e12
-        roof = {"kernel": "knn_tc_kernel (tcgen05 BF16 + re-rank)", "bound": "tensor", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": profile_traffic("knn_tc"),
-                "peak_source": pk_kind + " bf16 burst", "duration_ms": st["ms_knn"]}
-    # SGD against the HBM byte model: 8 B/edge/epoch + 4*dim*(m+1) B/positive + 8*dim*n B/epoch
+    # per-kernel live times (ms per step) and their roofline fractions
+    kernels = {}
+    for name, (tot, cnt) in prof.items():
+        per = tot / args.steps
+        bound, work, unit = kernel_work(name, c, st, n_amb)
+        rec = {"ms_per_step": per, "launches_per_step": cnt / args.steps, "share_of_step": per / ms}
+        if bound == "tensor":
+            peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+            rec.update(bound="tensor", achieved=work / (per / 1e3) / 1e12, peak=peak, unit="TFLOP/s")
+        elif bound == "hbm":
+            rec.update(bound="hbm", achieved=work / (per / 1e3) / 1e9, peak=pk["hbm_gbs"], unit="GB/s")
+        if bound:
+            rec["frac"] = rec["achieved"] / rec["peak"]
+        kernels[name] = rec
+    dom = max(kernels, key=lambda kk: kernels[kk]["ms_per_step"]) if kernels else None
+    roof = None
+    if dom:
+        r = kernels[dom]
+        bound, work, unit = kernel_work(dom, c, st, n_amb)
+        traffic, tsrc = profile_traffic(dom)
+        launches_dom = max(1.0, r["launches_per_step"])
+        roof = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"), "peak": r.get("peak"),
+                "unit": r.get("unit"), "frac": r.get("frac"),
+                "traffic": traffic,
+                "traffic_source": tsrc, "algorithmic_per_launch": (work / launches_dom) if work else None,
+                "algorithmic_unit": unit, "duration_ms_per_launch": r["ms_per_step"] / launches_dom,
+                "peak_source": pk_kind + (" bf16 sustained (kernel timed inside a long step)"
+                                          if r.get("bound") == "tensor" else " HBM copy bandwidth")}
     sgd_bytes = 8.0 * st["nnz"] * (N - 1) + 4 * 2 * 6 * positives + 8 * 2 * n * (N - 1)
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (bf16 tensor-core operands)",
         "data": "synthetic",
         "config": {"workload": f"{args.config} lowrank {n}x{d} k={k} 2-D {N} epochs fit + trust(k={trust_k})",
                    "knn_mode": args.knn_mode, "sgd_mode": args.sgd_mode,
                    "l2": "flushed (256 MiB write) between timed steps; X = %.0f MB > L2" % (n * d * 4 / 1e6),
                    "parallelism": f"kNN+trust rows sharded x{world}" if world > 1 else "1 GPU"},
         "stages_ms": {"knn": st["ms_knn"], "smooth": st["ms_smooth"], "union": st["ms_union"],
-                      "init": st["ms_init"], "sgd": st["ms_sgd"], "fit_total": st["ms_total"],
-                      "trust": ms - st["ms_total"]},
-        "fit_s": st["ms_total"] / 1e3,
+                      "init": st["ms_init"], "sgd": st["ms_sgd"], "trust": st.get("ms_trust", 0.0),
+                      "total": st["ms_total"]},
+        "fit_s": (st["ms_total"] - st.get("ms_trust", 0.0)) / 1e3,
         "sgd_edge_updates_per_s": positives / sgd_s if sgd_s > 0 else None,
         "sgd_hbm_model_frac": (sgd_bytes / sgd_s / 1e9) / pk["hbm_gbs"] if sgd_s > 0 else None,
-        "positives": positives, "nnz": st["nnz"], "trustworthiness": T,
+        "positives": positives, "nnz": st["nnz"], "trustworthiness": T, "trust_ambiguous_pairs": n_amb,
         "roofline": roof,
+        "kernels": kernels,
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,
-        "peaks": {"source": pk_kind, "hbm_gbs": pk.get("hbm_gbs"), "bf16_tflops": pk.get("bf16_tflops")},
+        "peaks": {"source": pk_kind, "hbm_gbs": pk.get("hbm_gbs"), "bf16_tflops": pk.get("bf16_tflops"),
+                  "bf16_tflops_sustained": pk.get("bf16_tflops_sustained")},
     }
     if not args.no_cpu_baseline and world == 1:
-        t_cpu, parts, sample = oracle_step_estimate(np.ascontiguousarray(X_host.numpy()), k, N)
+        t_cpu, parts, sample = oracle_step_estimate(np.ascontiguousarray(X_host.numpy()), k, N, knn_rows=96,
+                                                    graph_rows=2000, sgd_epochs=30, trust_rows=96)
         line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample,
-                                "stages_s": parts}
+                                "stages_s": parts, "host_cpu": _cpu_model()}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical cores on the host)"
+    except OSError:
+        pass
+    return None
 
 
 def main():

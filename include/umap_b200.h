@@ -84,6 +84,8 @@ typedef struct {
     int32_t  knn_mode;             /* umap_knn_mode, default UMAP_KNN_EXACT_FP32             */
     int32_t  knn_candidates;       /* k' candidates per row before re-rank (TC mode), 32     */
     int32_t  transform_epochs;     /* 0 -> ceil(n_epochs / 3) (R15)                          */
+    int32_t  trust_k;              /* umap_fit only: > 0 -> also score the embedding with    */
+                                   /* T(trust_k) (a10, knn_mode) into umap_fit_stats; 0 skip */
 } umap_params;
 
 /* Per-stage device times (ms, CUDA events on `stream`) and graph statistics. */
@@ -95,6 +97,9 @@ typedef struct {
     float   a, b;           /* curve parameters used                                       */
     int32_t n_epochs;       /* N used                                                      */
     int32_t gpu_launches;   /* kernels launched by this call                               */
+    double  ms_trust;       /* p->trust_k > 0: device time of the trustworthiness stage    */
+    double  trustworthiness;/* p->trust_k > 0: T(trust_k) of the returned embedding, else 0 */
+    int64_t trust_penalty;  /* p->trust_k > 0: the integer penalty sum S of T (R16)         */
 } umap_fit_stats;
 
 /* Fill *p with the defaults above. */
@@ -219,6 +224,15 @@ UMAP_API int64_t     umap_kernel_launch_count(void);
 /* Diagnostics: pairs the calling thread's last tensor-mode trustworthiness call could not
  * certify from the tensor-core pass and re-checked exactly. */
 UMAP_API int64_t     umap_trust_ambiguous_count(void);
+/* Live per-kernel timing (bench.py's roofline): between umap_profile_begin() and
+ * umap_profile_end() every hot kernel launched by the calling thread is bracketed by a CUDA
+ * event pair on its own stream.  umap_profile_end synchronises those events, writes the
+ * summed milliseconds and launch count per slot into ms[n_slots] / launches[n_slots] (either
+ * may be NULL) and returns the number of slots the library defines; slot names come from
+ * umap_profile_slot_name(slot) ("" out of range).  Host-side only; never fails. */
+UMAP_API void        umap_profile_begin(void);
+UMAP_API int32_t     umap_profile_end(double* ms, int64_t* launches, int32_t n_slots);
+UMAP_API const char* umap_profile_slot_name(int32_t slot);
 /* Library version string. */
 UMAP_API const char* umap_version(void);
 

@@ -29,14 +29,15 @@ class UmapParams(ctypes.Structure):
                 ("n_epochs", c_int32), ("min_dist", c_float), ("spread", c_float),
                 ("negative_sample_rate", c_int32), ("learning_rate", c_float), ("repulsion_strength", c_float),
                 ("a", c_float), ("b", c_float), ("seed", c_uint64), ("sgd_mode", c_int32), ("knn_mode", c_int32),
-                ("knn_candidates", c_int32), ("transform_epochs", c_int32)]
+                ("knn_candidates", c_int32), ("transform_epochs", c_int32), ("trust_k", c_int32)]
 
 
 class UmapFitStats(ctypes.Structure):
     _fields_ = [("ms_knn", c_double), ("ms_smooth", c_double), ("ms_union", c_double), ("ms_init", c_double),
                 ("ms_sgd", c_double), ("ms_total", c_double), ("nnz", c_int64), ("positives", c_int64),
                 ("w_max", c_float), ("a", c_float), ("b", c_float), ("n_epochs", c_int32),
-                ("gpu_launches", c_int32)]
+                ("gpu_launches", c_int32), ("ms_trust", c_double), ("trustworthiness", c_double),
+                ("trust_penalty", c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -72,6 +73,9 @@ SIGNATURES = {
     "umap_kernel_launch_count": (c_int64, []),
     "umap_version": (ctypes.c_char_p, []),
     "umap_trust_ambiguous_count": (c_int64, []),
+    "umap_profile_begin": (None, []),
+    "umap_profile_end": (ctypes.c_int32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64), ctypes.c_int32]),
+    "umap_profile_slot_name": (ctypes.c_char_p, [ctypes.c_int32]),
 }
 
 _lib = None

@@ -43,7 +43,7 @@ def _any(t, dtype, name):
 
 def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0, negative_sample_rate=5,
            learning_rate=1.0, repulsion_strength=1.0, a=0.0, b=0.0, seed=0, sgd_mode="deterministic",
-           knn_mode="exact", knn_candidates=32, transform_epochs=0) -> UmapParams:
+           knn_mode="exact", knn_candidates=32, transform_epochs=0, trust_k=0) -> UmapParams:
     p = UmapParams()
     _lib.load().umap_params_default(ctypes.byref(p))
     p.n_neighbors, p.n_components, p.n_epochs = n_neighbors, n_components, n_epochs
@@ -52,7 +52,7 @@ def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0,
     p.seed = seed
     p.sgd_mode = SGD_MODES[sgd_mode] if isinstance(sgd_mode, str) else sgd_mode
     p.knn_mode = KNN_MODES[knn_mode] if isinstance(knn_mode, str) else knn_mode
-    p.knn_candidates, p.transform_epochs = knn_candidates, transform_epochs
+    p.knn_candidates, p.transform_epochs, p.trust_k = knn_candidates, transform_epochs, trust_k
     return p
 
 
@@ -64,7 +64,7 @@ def fit_ab(min_dist=0.1, spread=1.0):
 
 def fit(X, out=None, **kw):
     """umap_fit: X (n x d fp32, CUDA or CPU tensor) -> (Y, stats dict). Y lives where X lives
-    unless `out` is given."""
+    unless `out` is given.  trust_k > 0 also scores Y (stats["trustworthiness"])."""
     X = _any(X, torch.float32, "X")
     p = params(**kw)
     n, d = X.shape
@@ -244,6 +244,21 @@ def kernel_launch_count():
 def trust_ambiguous_count():
     """pairs the last tensor-mode trust call re-checked exactly (diagnostic)."""
     return int(_lib.load().umap_trust_ambiguous_count())
+
+
+def profile_begin():
+    """start live per-kernel CUDA-event timing of this thread's launches"""
+    _lib.load().umap_profile_begin()
+
+
+def profile_end():
+    """stop timing; {kernel slot name: (total ms, launches)} for every slot that ran"""
+    L = _lib.load()
+    n = 32
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    k = min(n, int(L.umap_profile_end(ms, cnt, n)))
+    return {L.umap_profile_slot_name(i).decode(): (ms[i], int(cnt[i])) for i in range(k) if cnt[i]}
 
 
 def version():

@@ -41,6 +41,18 @@ static thread_local std::string g_last_error;
 static thread_local int64_t g_launches = 0;
 
 void set_last_error(const std::string& s) { g_last_error = s; }
+
+// ---- live per-kernel timing (ProfScope, common.cuh)
+struct ProfRec { int slot; cudaEvent_t e0, e1; };
+static thread_local bool g_prof_on = false;
+static thread_local std::vector<ProfRec> g_prof;
+bool profiling_enabled() { return g_prof_on; }
+void profile_record(int slot, cudaEvent_t e0, cudaEvent_t e1) { g_prof.push_back({slot, e0, e1}); }
+static const char* const k_prof_names[PROF_NSLOTS] = {
+    "knn_tc_kernel (kNN candidates)", "rerank_kernel", "knn_tc_kernel (trust ranks)", "rank_fix_kernel",
+    "thresholds_warp_kernel", "grid_knn_kernel", "smooth_knn_kernel", "fuzzy union (5 kernels)",
+    "sgd_persistent_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
+    "transform_sgd_kernel"};
 void count_launch(int n) { g_launches += n; }
 
 umap_status cuda_status(cudaError_t e, const char* what)
@@ -208,6 +220,9 @@ umap_status resolve(const umap_params* in, int64_t n, umap_params* out)
     return UMAP_OK;
 }
 
+umap_status trust_device(const float* X, int d, const float* Y, int d_emb, int64_t n, int k, int knn_mode,
+                         double* T, int64_t* penalty, cudaStream_t s);
+
 umap_status run_knn(const umap_params* p, const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k,
                     int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
                     float* dist, cudaStream_t s)
@@ -233,6 +248,37 @@ const char* umap_version(void) { return "umap-b200 0.1 (sm_100a)"; }
 int64_t umap_kernel_launch_count(void) { return g_launches; }
 
 int64_t umap_trust_ambiguous_count(void) { return last_rank_ambiguous(); }
+
+void umap_profile_begin(void)
+{
+    for (auto& r : g_prof) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+    g_prof.clear();
+    g_prof_on = true;
+}
+
+int32_t umap_profile_end(double* ms, int64_t* launches, int32_t n_slots)
+{
+    g_prof_on = false;
+    for (int i = 0; i < n_slots; ++i) { if (ms) ms[i] = 0.0; if (launches) launches[i] = 0; }
+    for (auto& r : g_prof) {
+        float t = 0.f;
+        if (cudaEventSynchronize(r.e1) == cudaSuccess && cudaEventElapsedTime(&t, r.e0, r.e1) == cudaSuccess &&
+            r.slot < n_slots) {
+            if (ms) ms[r.slot] += t;
+            if (launches) launches[r.slot] += 1;
+        }
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    cudaGetLastError();
+    g_prof.clear();
+    return PROF_NSLOTS;
+}
+
+const char* umap_profile_slot_name(int32_t slot)
+{
+    return (slot >= 0 && slot < PROF_NSLOTS) ? k_prof_names[slot] : "";
+}
 
 const char* umap_last_error(void) { return g_last_error.c_str(); }
 
@@ -576,10 +622,18 @@ umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_params* p_
     UMAP_TRY(run_knn(&p, Xd.p, n, Xd.p, n, d, k, 0, 1, 0, 0, idx.as<int32_t>(), dist.as<float>(), s));
     st.ms_knn = tm.lap();
     UMAP_TRY(fit_from_knn(idx.as<int32_t>(), dist.as<float>(), n, p, Yd.p, st, tm, s));
+    if (p.trust_k > 0) {  // a10 on the device-resident X and Y (no second staging of X)
+        if (2 * (int64_t)p.trust_k >= n || p.trust_k > 64) {
+            set_last_error("trust_k: 1 <= trust_k < n/2, trust_k <= 64");
+            return UMAP_ERR_K_OUT_OF_RANGE;
+        }
+        UMAP_TRY(trust_device(Xd.p, d, Yd.p, dim, n, p.trust_k, p.knn_mode, &st.trustworthiness, &st.trust_penalty, s));
+        st.ms_trust = tm.lap();
+    }
     UMAP_TRY(Yd.finish(s));
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
     double t_post = tm.lap();
-    st.ms_total = t_pre + st.ms_knn + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + t_post;
+    st.ms_total = t_pre + st.ms_knn + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + st.ms_trust + t_post;
     st.gpu_launches = (int32_t)(g_launches - launches0);
     if (stats) *stats = st;
     return UMAP_OK;
@@ -671,20 +725,34 @@ umap_status umap_trustworthiness(const float* X, int32_t d, const float* Y, int3
     DevIn Xd, Yd;
     UMAP_TRY(Xd.make(X, (size_t)n * d, s));
     UMAP_TRY(Yd.make(Y, (size_t)n * d_emb, s));
+    return trust_device(Xd.p, d, Yd.p, d_emb, n, k, knn_mode, T, penalty, s);
+}
+
+}  // extern "C"
+
+namespace umapb200 {
+namespace {
+
+// a10 on device-resident X (n x d) and Y (n x d_emb): embedding kNN, then the input-space
+// rank penalty S and T = 1 - 2 S / (n k (2n - 3k - 1)) (R16).
+umap_status trust_device(const float* Xd, int d, const float* Yd, int d_emb, int64_t n, int k, int knn_mode,
+                         double* T, int64_t* penalty, cudaStream_t s)
+{
     Scratch eidx, edist;
     UMAP_TRY(eidx.alloc(sizeof(int32_t) * (size_t)n * k, s));
     UMAP_TRY(edist.alloc(sizeof(float) * (size_t)n * k, s));
     {
         umap_params pe;
         umap_params_default(&pe);
-        UMAP_TRY(run_knn(&pe, Yd.p, n, Yd.p, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
+        UMAP_TRY(run_knn(&pe, Yd, n, Yd, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
     }
     int64_t S = 0;
-    UMAP_TRY(trust_penalty(Xd.p, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, s));
+    UMAP_TRY(trust_penalty(Xd, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, s));
     const double nn = (double)n, kk = (double)k;
     *T = 1.0 - (2.0 / (nn * kk * (2.0 * nn - 3.0 * kk - 1.0))) * (double)S;
     if (penalty) *penalty = S;
     return UMAP_OK;
 }
 
-}  // extern "C"
+}  // namespace
+}  // namespace umapb200

@@ -32,6 +32,35 @@ void count_launch(int n = 1);
         if (_e != cudaSuccess) return ::umapb200::cuda_status(_e, name); \
     } while (0)
 
+// ---------------------------------------------------------------- live kernel timing
+// Optional per-kernel CUDA-event timing (umap_profile_begin / umap_profile_end): when
+// enabled, a ProfScope records an event pair around one launch on its stream.
+enum ProfSlot {
+    PROF_KNN_TC = 0, PROF_RERANK, PROF_TRUST_TC, PROF_RANK_FIX, PROF_THRESHOLDS, PROF_GRID_KNN,
+    PROF_SMOOTH_KNN, PROF_UNION, PROF_SGD, PROF_KNN_EXACT, PROF_TRUST_EXACT, PROF_TRANSFORM_SGD, PROF_NSLOTS
+};
+bool profiling_enabled();
+void profile_record(int slot, cudaEvent_t e0, cudaEvent_t e1);
+struct ProfScope {
+    int slot;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ProfScope(int sl, cudaStream_t st) : slot(sl), s(st)
+    {
+        if (profiling_enabled() && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
+            cudaEventRecord(e0, s);
+        else
+            e0 = e1 = nullptr;
+    }
+    ~ProfScope()
+    {
+        if (e0) {
+            cudaEventRecord(e1, s);
+            profile_record(slot, e0, e1);  // ownership of the events moves to the profile table
+        }
+    }
+};
+
 inline int num_sms()
 {
     static int sms = 0;
@@ -126,6 +155,7 @@ __device__ __forceinline__ float exact_d2(const float* x, const float* y, int d)
     }
     return s;
 }
+
 
 // ascending bitonic sort of 32 (key, id) pairs across a warp (lane i ends with rank i)
 __device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)

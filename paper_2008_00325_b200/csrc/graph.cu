@@ -242,6 +242,7 @@ umap_status smooth_knn(const float* dist, const int32_t* idx, int64_t n, int k, 
                                            (int)(SK_WARPS * 32 * 65 * 8)));
         configured = true;
     }
+    ProfScope ps(PROF_SMOOTH_KNN, s);
     smooth_knn_kernel<<<ceil_div(n, 32 * SK_WARPS), 32 * SK_WARPS, smem_alloc, s>>>(dist, idx, n, k, rho, sigma,
                                                                                    w, col_sorted);
     UMAP_LAUNCH_CHECK("smooth_knn_kernel");
@@ -292,6 +293,7 @@ umap_status fuzzy_union(const int32_t* acol, const float* aw, int64_t n, int k, 
     UMAP_TRY(cnt.alloc(sizeof(int32_t) * (size_t)n, s));
     UMAP_CUDA_TRY(cudaMemsetAsync(deg.p, 0, sizeof(int32_t) * n, s));
     UMAP_CUDA_TRY(cudaMemsetAsync(cursor.p, 0, sizeof(int32_t) * n, s));
+    ProfScope ps(PROF_UNION, s);  // the whole union (includes one nnz read-back)
     indeg_kernel<<<ceil_div(m, 256), 256, 0, s>>>(acol, m, deg.as<int32_t>());
     UMAP_LAUNCH_CHECK("indeg_kernel");
     UMAP_TRY(exclusive_scan<int32_t>(deg.as<int32_t>(), n, tptr.as<int64_t>(), s));

@@ -216,6 +216,7 @@ umap_status launch_tiles_t(const TileArgs& a, int n_splits, cudaStream_t s)
         configured = true;
     }
     dim3 grid(ceil_div(a.nq, BM), n_splits);
+    ProfScope ps(MODE == 0 ? PROF_KNN_EXACT : PROF_TRUST_EXACT, s);
     dist_tile_kernel<KMAX, MODE><<<grid, NT, smem, s>>>(a);
     UMAP_LAUNCH_CHECK("dist_tile_kernel");
     return UMAP_OK;

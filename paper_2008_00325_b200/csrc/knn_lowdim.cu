@@ -185,6 +185,7 @@ umap_status knn_grid2d(const float* Y, int64_t n, int k, int out_squared, int32_
     cell_fill_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Y, n, cell_of.as<int32_t>(), start.as<int64_t>(),
                                                        cursor.as<int32_t>(), pid.as<int32_t>(), pxy.as<float2>());
     UMAP_LAUNCH_CHECK("cell_fill_kernel");
+    ProfScope ps(PROF_GRID_KNN, s);
     if (k <= 16)
         grid_knn_kernel<16><<<ceil_div(n, 128), 128, 0, s>>>(pxy.as<float2>(), pid.as<int32_t>(), start.as<int64_t>(),
                                                              box.as<float>(), G, n, k, out_squared, idx, dist);

@@ -208,17 +208,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
+            // MODE 1 (split operands, rows [hi | lo] of 2 KB columns): per K slab two stages,
+            // the hi parts (A_hi, B_hi) then the lo parts (A_lo, B_lo)
+            constexpr int PARTS = MODE == 1 ? 2 : 1;
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
                 const int y_r = (int)(r_lo + (int64_t)t * TC_BN);
-                for (int kb = 0; kb < KB; ++kb, ++g) {
-                    const int s = g % TC_STAGES;
-                    const uint32_t ph = (g / TC_STAGES) & 1;
-                    mbar_wait(empty0 + 8 * s, ph ^ 1);
-                    const uint32_t dst = smem_u32(stage_base + s * STAGE_BYTES);
-                    mbar_expect_tx(full0 + 8 * s, STAGE_BYTES);
-                    tma_load_2d(dst, &map_q, kb * TC_BK, (int)q0, full0 + 8 * s);
-                    tma_load_2d(dst + A_BYTES, &map_r, kb * TC_BK, y_r, full0 + 8 * s);
+                for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+                    for (int part = 0; part < PARTS; ++part, ++g) {
+                        const int s = g % TC_STAGES;
+                        const uint32_t ph = (g / TC_STAGES) & 1;
+                        mbar_wait(empty0 + 8 * s, ph ^ 1);
+                        const uint32_t dst = smem_u32(stage_base + s * STAGE_BYTES);
+                        const int x = (part * KB + kb) * TC_BK;
+                        mbar_expect_tx(full0 + 8 * s, STAGE_BYTES);
+                        tma_load_2d(dst, &map_q, x, (int)q0, full0 + 8 * s);
+                        tma_load_2d(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s);
+                    }
                 }
             }
         }
@@ -231,7 +238,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 mbar_wait(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(b * TC_BN);
-                for (int kb = 0; kb < KB; ++kb, ++g) {
+                for (int kb = 0; kb < KB; ++kb) {
                     const int s = g % TC_STAGES;
                     const uint32_t ph = (g / TC_STAGES) & 1;
                     mbar_wait(full0 + 8 * s, ph);
@@ -242,6 +249,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     for (int kk = 0; kk < TC_BK / 16; ++kk) {
                         if (!(a.debug & 2)) umma_bf16(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
                                   (kb | kk) != 0);
+                    }
+                    ++g;
+                    if constexpr (MODE == 1) {
+                        // lo stage: hi_q . lo_r (A of the hi stage, B of the lo stage) and
+                        // lo_q . hi_r (A of the lo stage, B of the hi stage) into the same accumulator
+                        const int s2 = g % TC_STAGES;
+                        const uint32_t ph2 = (g / TC_STAGES) & 1;
+                        mbar_wait(full0 + 8 * s2, ph2);
+                        tc_fence_after();
+                        const uint32_t a2 = smem_u32(stage_base + s2 * STAGE_BYTES);
+                        const uint32_t b2 = a2 + A_BYTES;
+#pragma unroll
+                        for (int kk = 0; kk < TC_BK / 16; ++kk) {
+                            umma_bf16(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b2 + kk * 32), 1u);
+                            umma_bf16(tmem_d, umma_desc_sw128(a2 + kk * 32), umma_desc_sw128(b_addr + kk * 32), 1u);
+                        }
+                        umma_commit(empty0 + 8 * s2);
+                        ++g;
                     }
                     umma_commit(empty0 + 8 * s);  // smem slot free once these MMAs have read it
                 }
@@ -507,18 +532,18 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
 }
 
 // split-BF16 operands for the RANK mode: x_c = x - mean (fp32), hi = bf16(x_c),
-// lo = bf16(x_c - hi).  Queries get [hi | hi | lo], references [hi | lo | hi] along K, so one
-// GEMM over K' = 3 d_pad yields hi.hi + hi.lo + lo.hi (x.y to ~2^-17 relative); norms are
-// the fp32 sums of x_c^2.
+// lo = bf16(x_c - hi), row layout [hi | lo] (2 d_pad columns).  The RANK kernel issues
+// hi.hi + hi.lo + lo.hi into one accumulator from the hi and lo K slabs (x.y to ~2^-16
+// relative); norms are the fp32 sums of x_c^2.
 __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
-                                  const double* __restrict__ colsum, double inv_n, int ref_layout,
+                                  const double* __restrict__ colsum, double inv_n,
                                   __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms)
 {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     float acc = 0.0f;
-    __nv_bfloat16* o = Xs + row * (int64_t)(3 * d_pad);
+    __nv_bfloat16* o = Xs + row * (int64_t)(2 * d_pad);
     for (int f = lane; f < d_pad; f += 32) {
         __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
         if (f < d) {
@@ -528,8 +553,7 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
             acc = fmaf(c, c, acc);
         }
         o[f] = hi;
-        o[d_pad + f] = ref_layout ? lo : hi;
-        o[2 * d_pad + f] = ref_layout ? hi : lo;
+        o[d_pad + f] = lo;
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
@@ -543,14 +567,23 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
 // row's two lists (one per column half) hold reference ids; each lane takes pairs,
 // computes the exact R2 key and its bucket (first threshold it is below), the warp
 // accumulates a shared histogram and adds it to the row's certain counts.
-__global__ void rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
-                                const int32_t* __restrict__ amb, const int* __restrict__ amb_count, int cap_row,
-                                const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
-                                int64_t index_offset, int32_t* __restrict__ hist)
+// Exact re-check of the RANK mode's ambiguous pairs (R16).  Warp per query row: the
+// row's two lists (one per column half) hold reference ids; each lane takes pairs,
+// computes the exact R2 key (its own sequential fmaf chain, float4 loads) and its bucket
+// (first threshold it is below), the warp accumulates a shared histogram and adds it to
+// the row's certain counts.  (A warp-cooperative variant that stages the 32 candidate
+// rows through shared memory with coalesced loads / cp.async measured 2x slower at C2:
+// 4-byte LDGSTS and per-row LDG+STS are LSU-issue bound.)
+constexpr int RF_WARPS = 8;
+__global__ void __launch_bounds__(32 * RF_WARPS)
+rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
+                const int32_t* __restrict__ amb, const int* __restrict__ amb_count, int cap_row,
+                const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
+                int64_t index_offset, int32_t* __restrict__ hist)
 {
-    __shared__ int h[8][16];
+    __shared__ int h[RF_WARPS][16];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t q = (int64_t)blockIdx.x * 8 + warp;
+    const int64_t q = (int64_t)blockIdx.x * RF_WARPS + warp;
     if (q >= nq) return;
     if (lane < 16) h[warp][lane] = 0;
     __syncwarp();
@@ -695,6 +728,7 @@ umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs
                                            (int)smem));
         configured = true;
     }
+    ProfScope ps(MODE == 0 ? PROF_KNN_TC : PROF_TRUST_TC, s);
     knn_tc_kernel<KC, ST, MODE><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
     UMAP_LAUNCH_CHECK("knn_tc_kernel");
     return UMAP_OK;
@@ -773,6 +807,7 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
                             md.as<float>(), s));
         cand = mi.as<int32_t>();
     }
+    ProfScope ps(PROF_RERANK, s);
     rerank_kernel<<<ceil_div(nq * 32, 256), 256, 0, s>>>(Xq, Xr, d, nq, cand, kc, index_offset, k, out_squared, idx,
                                                          dist);
     UMAP_LAUNCH_CHECK("rerank_kernel");
@@ -792,7 +827,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     if (rows == 0) return UMAP_OK;
     if (k > TC_KT) { *overflow = 1; return UMAP_OK; }
     const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
-    const int dk = 3 * d_pad;
+    const int dk = 2 * d_pad;
     Scratch colsum, xr, rn, xq, qn, amb, ambc;
     UMAP_TRY(colsum.alloc(sizeof(double) * d, s));
     UMAP_CUDA_TRY(cudaMemsetAsync(colsum.p, 0, sizeof(double) * d, s));
@@ -803,13 +838,13 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     }
     UMAP_TRY(xr.alloc(sizeof(__nv_bfloat16) * (size_t)n * dk, s));
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)n, s));
-    split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n, 1,
+    split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n,
                                                           xr.as<__nv_bfloat16>(), rn.as<float>());
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
     split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X + row_begin * (int64_t)d, rows, d, d_pad,
-                                                             colsum.as<double>(), 1.0 / (double)n, 0,
+                                                             colsum.as<double>(), 1.0 / (double)n,
                                                              xq.as<__nv_bfloat16>(), qn.as<float>());
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     CUtensorMap map_q, map_r;
@@ -820,16 +855,19 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * 2 * cap, s));
     UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * 2, s));
     TcArgs a{};
-    a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = dk / TC_BK; a.kc = 0;
+    a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = d_pad / TC_BK; a.kc = 0;
     a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
     a.thr_d2 = thr_d2; a.k = k; a.margin = 5e-4f;
     if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
     a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     a.amb_count = ambc.as<int>();
     UMAP_TRY((launch_tc<32, 4, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
-    rank_fix_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),
+    {
+    ProfScope ps(PROF_RANK_FIX, s);
+    rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),
                                                       ambc.as<int>(), cap, thr_d2, thr_id, k, 0, hist);
     UMAP_LAUNCH_CHECK("rank_fix_kernel");
+    }
     std::vector<int> counts((size_t)rows * 2);
     UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * 2, cudaMemcpyDeviceToHost, s));
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));

@@ -487,6 +487,7 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
     const int64_t want = (A.n_chunks + CPB - 1) / CPB;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, max_blocks));
     void* args[] = {&A};
+    ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * SGD_WARPS), args, 0, s));
     UMAP_LAUNCH_CHECK("sgd_persistent_kernel");
     return UMAP_OK;
@@ -526,6 +527,7 @@ umap_status launch_transform_t(const int32_t* idx, const float* w, int64_t nq, i
                                float* Yq, const float* wmax, const umap_params* p, int nt, int eb, int ee,
                                int64_t q_offset, int init, cudaStream_t s)
 {
+    ProfScope ps(PROF_TRANSFORM_SGD, s);
     transform_sgd_kernel<DIM, KMAX><<<ceil_div(nq, 128), 128, 0, s>>>(
         idx, w, nq, k, Ytr, ntr, Yq, wmax, p->a, p->b, p->repulsion_strength, p->learning_rate, nt, eb, ee,
         p->negative_sample_rate, (uint32_t)p->seed, (uint32_t)(p->seed >> 32), q_offset, init);

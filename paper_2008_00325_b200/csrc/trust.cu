@@ -99,6 +99,7 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
     UMAP_TRY(total.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(total.p, 0, sizeof(unsigned long long), s));
     if (k <= 32) {
+        ProfScope ps(PROF_THRESHOLDS, s);
         thresholds_warp_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X, d, emb_idx, rows, row_begin, k,
                                                                         thr_d.as<float>(), thr_i.as<int32_t>());
         UMAP_LAUNCH_CHECK("thresholds_warp_kernel");

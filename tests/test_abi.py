@@ -38,14 +38,36 @@ def test_library_exports_every_declared_symbol(lib):
     assert set(lib.SIGNATURES) == set(_declared_symbols())
 
 
-def test_struct_layout_matches_header(lib):
-    # offsets follow C natural alignment; the seed field forces 8-byte alignment
-    assert ctypes.sizeof(lib.UmapParams) == 72
-    assert lib.UmapParams.seed.offset == 48
-    assert ctypes.sizeof(lib.UmapFitStats) == 88
+def _c_layout(struct, fields):
+    """sizeof/offsetof of a header struct as gcc lays it out (the C side of the ABI)."""
+    import subprocess
+    import tempfile
+    body = "".join(f'printf("%zu\\n", offsetof({struct}, {f}));' for f in fields)
+    src = (f'#include <stdio.h>\n#include <stddef.h>\n#include "umap_b200.h"\n'
+           f'int main(void){{printf("%zu\\n", sizeof({struct}));{body}return 0;}}\n')
+    with tempfile.TemporaryDirectory() as td:
+        c, exe = os.path.join(td, "probe.c"), os.path.join(td, "probe")
+        open(c, "w").write(src)
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe])
+        vals = [int(x) for x in subprocess.check_output([exe]).split()]
+    return vals[0], dict(zip(fields, vals[1:]))
+
+
+@pytest.mark.parametrize("cname,pyname", [("umap_params", "UmapParams"), ("umap_fit_stats", "UmapFitStats")])
+def test_struct_layout_matches_header(lib, cname, pyname):
+    cls = getattr(lib, pyname)
+    fields = [f for f, _ in cls._fields_]
+    size, offs = _c_layout(cname, fields)
+    assert ctypes.sizeof(cls) == size
+    for f in fields:
+        assert getattr(cls, f).offset == offs[f], f
+
+
+def test_params_defaults(lib):
     p = lib.UmapParams()
     lib.load().umap_params_default(ctypes.byref(p))
-    assert p.struct_size == 72 and p.n_neighbors == 15 and p.n_components == 2 and p.negative_sample_rate == 5
+    assert p.struct_size == ctypes.sizeof(lib.UmapParams) and p.n_neighbors == 15 and p.n_components == 2
+    assert p.negative_sample_rate == 5 and p.trust_k == 0
     assert p.sgd_mode == lib.SGD_DETERMINISTIC and p.knn_candidates == 32
 
 
