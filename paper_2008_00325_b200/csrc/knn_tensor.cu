@@ -119,6 +119,77 @@ __device__ __forceinline__ void umma_commit(uint32_t bar)
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) helpers: the pair's MMA is issued by the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t cluster_ctarank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr)
+{
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+// TMA load whose completion bytes go to the leader CTA's mbarrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar_cluster)
+        : "memory");
+}
+// instruction descriptor with M = 256 (pair), N = 256
+constexpr uint32_t IDESC_PAIR = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_BN >> 3) << 17) |
+                                ((uint32_t)((2 * TC_BM) >> 4) << 24);
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC_PAIR), "r"(accumulate)
+        : "memory");
+}
+// commit: arrive once on the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"((uint16_t)3) : "memory");
+}
+template <int CG> __device__ __forceinline__ void umma_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc)
+{
+    if constexpr (CG == 2) umma_bf16_pair(tmem_d, adesc, bdesc, acc);
+    else umma_bf16(tmem_d, adesc, bdesc, acc);
+}
+template <int CG> __device__ __forceinline__ void umma_arrive(uint32_t bar)
+{
+    if constexpr (CG == 2) umma_commit_pair(bar);
+    else umma_commit(bar);
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
 {
     uint32_t r[32];
@@ -161,16 +232,25 @@ struct TcArgs {
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
 
-template <int KC, int TC_STAGES, int MODE>
+// CG = 1: one CTA, MMA M = 128.  CG = 2: a CTA pair (cluster of 2 along the query blocks)
+// runs tcgen05.mma.cta_group::2 with M = 256: each CTA loads its own 128 query rows and
+// half (128 rows) of the 256-row reference tile, so the L2 -> SMEM bytes per MMA flop drop
+// by a third; the leader (rank 0) issues the MMAs, each CTA's TMEM holds its 128 rows x
+// 256 columns, and each CTA's epilogue filters its own rows exactly as for CG = 1.
+template <int KC, int TC_STAGES, int MODE, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_r, TcArgs a)
 {
+    constexpr uint32_t B_ROWS = TC_BN / CG;                     // reference rows loaded by this CTA
+    constexpr uint32_t STAGE_C = A_BYTES + B_ROWS * TC_BK * 2;  // bytes per stage per CTA
     extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     uint8_t* smem = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* stage_base = smem;                                     // TC_STAGES x (A | B)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);  // full[S], empty[S], tfull[2], tempty[2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_C);  // full[S], empty[S], tfull[2], tempty[2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TC_STAGES + 4);
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t q0 = (int64_t)blockIdx.x * TC_BM;
@@ -189,19 +269,26 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, TC_EPI_WARPS);
+            mbar_init(tempty0 + 8 * b, CG * TC_EPI_WARPS);  // the epilogue warps of every CTA of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_q) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_r) : "memory");
     }
-    if (warp == 1) {  // TMEM: 512 columns = two 128x256 fp32 accumulators
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (warp == 1) {  // TMEM: 512 columns = two 128x256 fp32 accumulators (per CTA)
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -220,22 +307,31 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         const int s = g % TC_STAGES;
                         const uint32_t ph = (g / TC_STAGES) & 1;
                         mbar_wait(empty0 + 8 * s, ph ^ 1);
-                        const uint32_t dst = smem_u32(stage_base + s * STAGE_BYTES);
+                        const uint32_t dst = smem_u32(stage_base + s * STAGE_C);
                         const int x = (part * KB + kb) * TC_BK;
-                        mbar_expect_tx(full0 + 8 * s, STAGE_BYTES);
-                        tma_load_2d(dst, &map_q, x, (int)q0, full0 + 8 * s);
-                        tma_load_2d(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s);
+                        if constexpr (CG == 2) {
+                            // both CTAs' bytes complete on the leader's full barrier
+                            if (leader) mbar_expect_tx(full0 + 8 * s, CG * STAGE_C);
+                            const uint32_t fb = mapa_shared(full0 + 8 * s, 0);
+                            tma_load_2d_cg2(dst, &map_q, x, (int)q0, fb);
+                            tma_load_2d_cg2(dst + A_BYTES, &map_r, x, y_r + (int)(rank * B_ROWS), fb);
+                        } else {
+                            mbar_expect_tx(full0 + 8 * s, STAGE_C);
+                            tma_load_2d(dst, &map_q, x, (int)q0, full0 + 8 * s);
+                            tma_load_2d(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s);
+                        }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
+        if (lane == 0 && leader) {
+            // ------------------------------------------------ MMA issuer (leader CTA of a pair)
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
                 const int b = t & 1;
-                mbar_wait(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
+                if constexpr (CG == 2) mbar_wait_cluster(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
+                else mbar_wait(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(b * TC_BN);
                 for (int kb = 0; kb < KB; ++kb) {
@@ -243,11 +339,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const uint32_t ph = (g / TC_STAGES) & 1;
                     mbar_wait(full0 + 8 * s, ph);
                     tc_fence_after();
-                    const uint32_t a_addr = smem_u32(stage_base + s * STAGE_BYTES);
+                    const uint32_t a_addr = smem_u32(stage_base + s * STAGE_C);
                     const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < TC_BK / 16; ++kk) {
-                        if (!(a.debug & 2)) umma_bf16(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                        if (!(a.debug & 2)) umma_mma<CG>(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
                                   (kb | kk) != 0);
                     }
                     ++g;
@@ -258,19 +354,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         const uint32_t ph2 = (g / TC_STAGES) & 1;
                         mbar_wait(full0 + 8 * s2, ph2);
                         tc_fence_after();
-                        const uint32_t a2 = smem_u32(stage_base + s2 * STAGE_BYTES);
+                        const uint32_t a2 = smem_u32(stage_base + s2 * STAGE_C);
                         const uint32_t b2 = a2 + A_BYTES;
 #pragma unroll
                         for (int kk = 0; kk < TC_BK / 16; ++kk) {
-                            umma_bf16(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b2 + kk * 32), 1u);
-                            umma_bf16(tmem_d, umma_desc_sw128(a2 + kk * 32), umma_desc_sw128(b_addr + kk * 32), 1u);
+                            umma_mma<CG>(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b2 + kk * 32), 1u);
+                            umma_mma<CG>(tmem_d, umma_desc_sw128(a2 + kk * 32), umma_desc_sw128(b_addr + kk * 32), 1u);
                         }
-                        umma_commit(empty0 + 8 * s2);
+                        umma_arrive<CG>(empty0 + 8 * s2);
                         ++g;
                     }
-                    umma_commit(empty0 + 8 * s);  // smem slot free once these MMAs have read it
+                    umma_arrive<CG>(empty0 + 8 * s);  // smem slot free (in both CTAs) once these MMAs have read it
                 }
-                umma_commit(tfull0 + 8 * b);      // accumulator b complete
+                umma_arrive<CG>(tfull0 + 8 * b);  // accumulator b complete (in both CTAs)
             }
         }
     } else if constexpr (MODE == 1) {
@@ -297,7 +393,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         for (int t = 1; t < TC_KT; ++t) tmax = (t < k) ? thr[t] : tmax;
         const float c_m = a.margin;
         // shared histogram [half][t][row] after the ring region (ring stays untouched)
-        int32_t* Hs = reinterpret_cast<int32_t*>(stage_base + TC_STAGES * STAGE_BYTES + 8 * (2 * TC_STAGES + 4) + 16);
+        int32_t* Hs = reinterpret_cast<int32_t*>(stage_base + TC_STAGES * STAGE_C + 8 * (2 * TC_STAGES + 4) + 16);
 #pragma unroll
         for (int t = 0; t < TC_KT; ++t) Hs[(half * TC_KT + t) * TC_BM + row] = 0;
         asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
@@ -358,7 +454,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(tempty0 + 8 * b, 0));
+                else mbar_arrive(tempty0 + 8 * b);
+            }
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
         if (half == 0 && valid) {
@@ -441,7 +540,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty0 + 8 * b);
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(tempty0 + 8 * b, 0));
+                else mbar_arrive(tempty0 + 8 * b);
+            }
         }
         // merge the two halves of each row: half 1 publishes its list through smem (the
         // stage ring is idle now: every TMA load has been consumed by the last MMA)
@@ -483,10 +585,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs and both epilogues are done
+    else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        if constexpr (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
     }
 }
 
@@ -712,26 +818,62 @@ umap_status prep_bf16(const float* X, int64_t n, int d, int d_pad, const double*
 
 }  // namespace
 
-template <int KC, int ST, int MODE>
+template <int KC, int ST, int MODE, int CG>
 size_t knn_tc_smem_bytes()
 {
-    return 1024 + ST * STAGE_BYTES + 8 * (2 * ST + 4) + 16 + (MODE == 1 ? 2 * TC_KT * TC_BM * 4 + 16 : 0);
+    const size_t stage = A_BYTES + (size_t)(TC_BN / CG) * TC_BK * 2;
+    return 1024 + ST * stage + 8 * (2 * ST + 4) + 16 + (MODE == 1 ? 2 * TC_KT * TC_BM * 4 + 16 : 0);
 }
 
-template <int KC, int ST, int MODE = 0>
-umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
+// CTA-pair MMA (cta_group::2) unless UMAP_TC_CG=1 (A/B comparison knob)
+int tc_cg()
 {
-    const size_t smem = knn_tc_smem_bytes<KC, ST, MODE>();
+    static int cg = 0;
+    if (!cg) {
+        const char* e = getenv("UMAP_TC_CG");
+        cg = (e && atoi(e) == 1) ? 1 : 2;
+    }
+    return cg;
+}
+
+template <int KC, int ST, int MODE, int CG>
+umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
+{
+    const size_t smem = knn_tc_smem_bytes<KC, ST, MODE, CG>();
     static bool configured = false;
     if (!configured) {
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST, MODE, CG>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
     ProfScope ps(MODE == 0 ? PROF_KNN_TC : PROF_TRUST_TC, s);
-    knn_tc_kernel<KC, ST, MODE><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
+    if constexpr (CG == 2) {
+        grid.x = (grid.x + 1) & ~1u;  // whole pairs; a pair's second block may lie past n_q (masked)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        UMAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, knn_tc_kernel<KC, ST, MODE, CG>, mq, mr, a));
+    } else {
+        knn_tc_kernel<KC, ST, MODE, CG><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
+    }
     UMAP_LAUNCH_CHECK("knn_tc_kernel");
     return UMAP_OK;
+}
+
+template <int KC, int MODE>
+umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
+{
+    if (tc_cg() == 2) return launch_tc_t<KC, 6, MODE, 2>(mq, mr, a, grid, s);
+    return launch_tc_t<KC, 4, MODE, 1>(mq, mr, a, grid, s);
 }
 
 // Tensor-core candidate kNN + exact re-rank.  Centring uses the column means of the
@@ -774,7 +916,7 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     }
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, q16, nq, d_pad, TC_BM));
-    UMAP_TRY(make_map(&map_r, xr16.as<__nv_bfloat16>(), nr, d_pad, TC_BN));
+    UMAP_TRY(make_map(&map_r, xr16.as<__nv_bfloat16>(), nr, d_pad, TC_BN / tc_cg()));
 
     // reference splits so that the grid covers the GPU (split-R, like the exact kernel)
     const int64_t qblocks = (nq + TC_BM - 1) / TC_BM;
@@ -796,8 +938,8 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
         a.debug = dbg ? atoi(dbg) : 0;
     }
     const dim3 grid((unsigned)qblocks, n_splits);
-    if (kc <= 32) UMAP_TRY((launch_tc<32, 4>(map_q, map_r, a, grid, s)));
-    else UMAP_TRY((launch_tc<64, 4>(map_q, map_r, a, grid, s)));
+    if (kc <= 32) UMAP_TRY((launch_tc<32, 0>(map_q, map_r, a, grid, s)));
+    else UMAP_TRY((launch_tc<64, 0>(map_q, map_r, a, grid, s)));
     const int32_t* cand = ci.as<int32_t>();
     Scratch mi, md;
     if (n_splits > 1) {  // merge the per-split candidate lists by approximate key
@@ -849,7 +991,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
-    UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN));
+    UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN / tc_cg()));
     const int64_t qblocks = (rows + TC_BM - 1) / TC_BM;
     const int cap = 2048;
     UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * 2 * cap, s));
@@ -861,7 +1003,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
     a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     a.amb_count = ambc.as<int>();
-    UMAP_TRY((launch_tc<32, 4, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
+    UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
     ProfScope ps(PROF_RANK_FIX, s);
     rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),

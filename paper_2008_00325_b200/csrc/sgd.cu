@@ -30,6 +30,7 @@ struct SgdArgs {
     const int2* edges;       // per CSR entry {col, float_as_int(r)}, r = w / w_max (R9), built once
     int64_t n;
     int64_t n_chunks;        // ceil(n / VPW)
+    const int32_t* bounds;   // CPB == 0: CTA b owns chunks [bounds[b], bounds[b+1]) (edge-balanced)
     float* Y0;               // positions (Hogwild: in place)
     float* Y1;               // deterministic: ping-pong partner of Y0
     float a, b, gamma, alpha0;
@@ -238,16 +239,19 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
         // a CTA owns CPB consecutive chunks (VPW * CPB vertices); its warps take chunks from
         // the CTA's range through a shared-memory counter (dynamic balance inside the CTA,
         // no global work counter: thousands of grabs per epoch would serialise at L2)
-        const int n_br = (n_chunks + CPB - 1) / CPB;
+        // (CPB == 0: one edge-balanced range per CTA, precomputed)
+        const int n_br = CPB > 0 ? (n_chunks + CPB - 1) / CPB : (int)gridDim.x;
         for (int br = blockIdx.x; br < (A.debug & 1 ? 0 : n_br); br += gridDim.x) {
+          const int c_lo = CPB > 0 ? br * CPB : A.bounds[br];
+          const int c_hi = CPB > 0 ? min(n_chunks, c_lo + CPB) : A.bounds[br + 1];
           if (threadIdx.x == 0) s_ctr = 0;
           __syncthreads();
           for (;;) {
             int ci = 0;
             if (lane == 0) ci = atomicAdd(&s_ctr, 1);
             ci = __shfl_sync(0xffffffffu, ci, 0);
-            const int chunk = br * CPB + ci;
-            if (ci >= CPB || chunk >= n_chunks) break;
+            const int chunk = c_lo + ci;
+            if (chunk >= c_hi) break;
             const int v0 = chunk * VPW;
             const int nv = min(VPW, n - v0);
             // lane l < nv holds indptr[v0 + l]; the end is loaded separately (nv may be 32)
@@ -344,6 +348,27 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
     }
     // due_count is warp-uniform (every lane added the same ballot counts)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
+// Edge-balanced CTA ranges for the persistent SGD kernel: CTA b gets the chunks whose
+// cost prefix W(c) = indptr[c VPW] + 2 c VPW (edges + per-vertex work) starts in
+// [b W / G, (b + 1) W / G).  bounds[0] = 0, bounds[G] = n_chunks.
+__global__ void chunk_bounds_kernel(const int64_t* __restrict__ indptr, int64_t n, int vpw, int n_chunks, int G,
+                                    int32_t* __restrict__ bounds)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > G) return;
+    auto W = [&](int c) -> double {
+        const int64_t v = min((int64_t)c * vpw, n);
+        return (double)indptr[v] + 2.0 * (double)v;
+    };
+    const double target = W(n_chunks) * (double)b / (double)G;
+    int lo = 0, hi = n_chunks;  // first c with W(c) >= target
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (W(mid) < target) lo = mid + 1; else hi = mid;
+    }
+    bounds[b] = b == G ? n_chunks : lo;
 }
 
 __global__ void edge_records_kernel(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t nnz,
@@ -484,8 +509,16 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
         UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * SGD_WARPS, 0));
         max_blocks = std::max(1, per_sm) * num_sms();
     }
-    const int64_t want = (A.n_chunks + CPB - 1) / CPB;
+    const int64_t want = CPB > 0 ? (A.n_chunks + CPB - 1) / CPB : A.n_chunks;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, max_blocks));
+    Scratch bounds;
+    if (CPB == 0) {
+        UMAP_TRY(bounds.alloc(sizeof(int32_t) * (size_t)(grid + 1), s));
+        chunk_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(A.indptr, A.n, VPW, (int)A.n_chunks, grid,
+                                                                    bounds.as<int32_t>());
+        UMAP_LAUNCH_CHECK("chunk_bounds_kernel");
+        A.bounds = bounds.as<int32_t>();
+    }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * SGD_WARPS), args, 0, s));
@@ -511,7 +544,15 @@ umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
         case 2: return launch_sgd_t<DIM, DET, MC, 8, 3, 32>(A, s);
         case 3: return launch_sgd_t<DIM, DET, MC, 16, 3, 32>(A, s);
         case 4: return launch_sgd_t<DIM, DET, MC, 32, 3, 16>(A, s);
-        default: return launch_sgd_t<DIM, DET, MC, 16, 3, 16>(A, s);
+        case 5: return launch_sgd_t<DIM, DET, MC, 16, 3, 8>(A, s);
+        case 6: return launch_sgd_t<DIM, DET, MC, 16, 4, 4>(A, s);
+        case 7: return launch_sgd_t<DIM, DET, MC, 8, 3, 8>(A, s);
+        case 8: return launch_sgd_t<DIM, DET, MC, 16, 4, 8>(A, s);
+        case 9: return launch_sgd_t<DIM, DET, MC, 16, 3, 16>(A, s);  // the round-1 shape
+        case 10: return launch_sgd_t<DIM, DET, MC, 8, 4, 0>(A, s);
+        case 11: return launch_sgd_t<DIM, DET, MC, 32, 4, 0>(A, s);
+        case 12: return launch_sgd_t<DIM, DET, MC, 16, 3, 0>(A, s);
+        default: return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);  // measured best at C2 (tools/sgd_variants.py)
     }
 }
 
