@@ -37,7 +37,8 @@ struct SgdArgs {
     int32_t n_epochs, e_begin, e_end, m;
     uint32_t key0, key1;
     unsigned long long* positives;  // device counter of due directed edges
-    unsigned int* bar;       // grid barrier {count, generation}
+    unsigned int* bar;       // grid barrier counters (BAR_WORDS words)
+    const uint8_t* owner;    // per CSR entry: head vertex & 255 (its lane in the owning chunk)
     int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only
 };
 
@@ -198,15 +199,18 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, 
 }
 
 // grid-wide barrier between epochs (cooperative launch guarantees co-residency);
-// the gpu-scope fences order the epoch's writes and invalidate L1
-// monotonic arrival counter: barrier number k completes when the counter reaches
-// (k + 1) * gridDim.x (no reset, one release-add and acquire polling per CTA)
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int target)
+// the gpu-scope fences order the epoch's writes and invalidate L1.  Monotonic arrival
+// counter: barrier number k (1-based) completes when the counter reaches k * gridDim.x (no
+// reset, one release-add and acquire polling per CTA).  A two-level variant (8 group
+// counters on separate lines) measured no faster at 592 CTAs.
+constexpr size_t BAR_WORDS = 2;
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int k)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned int target = k * gridDim.x;
         unsigned int v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
@@ -258,7 +262,6 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
             const int64_t ptr_l = lane < nv ? __ldg(A.indptr + v0 + lane) : 0;
             const int64_t e_lo = __shfl_sync(0xffffffffu, ptr_l, 0);
             const int64_t e_hi = __ldg(A.indptr + v0 + nv);
-            const int32_t pr = (int32_t)(ptr_l - e_lo);   // row offsets relative to the chunk
             if (DET && lane < VPW) {
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) acc[warp][c][lane] = 0;
@@ -274,7 +277,8 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
                 if (act) process_edge<DIM, DET, MC>(A, Yr, Yw, epoch, alpha, v0 + hl, q_t[warp][lane], qa);
                 if (DET) {
                     // queued items are in CSR order, so equal owners are contiguous: segmented
-                    // sum over the warp, the last lane of each segment adds it (order-free int sum)
+                    // sum over the warp, the last lane of each segment adds it (order-free int sum;
+                    // measured faster than 64-bit shared atomics)
                     long long sv[DIM];
 #pragma unroll
                     for (int c = 0; c < DIM; ++c) sv[c] = qa[c];
@@ -298,18 +302,11 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
             int2 nrec = (e_lo + lane < e_hi) ? __ldg(A.edges + e_lo + lane) : make_int2(0, 0);
             for (int64_t base = e_lo; base < e_hi; base += 32) {
                 const int64_t e = base + lane;
-                const int32_t el = (int32_t)(e - e_lo);
                 const int2 rec = nrec;  // records are prefetched one 32-edge step ahead
                 if (base + 32 + lane < e_hi) nrec = __ldg(A.edges + base + 32 + lane);
                 const bool due = e < e_hi && edge_due(__int_as_float(rec.y), epoch);
-                // owner lane: largest l < nv with pr[l] <= el (shuffle binary search)
-                int lo = 0, hi = nv;
-#pragma unroll
-                for (int it = 0; it < (VPW > 16 ? 5 : (VPW > 8 ? 4 : 3)); ++it) {
-                    const int mid = (lo + hi) >> 1;
-                    const int32_t pm = __shfl_sync(0xffffffffu, pr, mid);
-                    if (hi - lo > 1) { if (pm <= el) lo = mid; else hi = mid; }
-                }
+                // owner lane of the edge's head vertex within the chunk (precomputed)
+                const int lo = due ? (int)(__ldg(A.owner + e) & (VPW - 1)) : 0;
                 const unsigned ballot = __ballot_sync(0xffffffffu, due);
                 due_count += __popc(ballot);
                 if (due) {
@@ -344,7 +341,7 @@ __global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(Sg
           }
           __syncthreads();
         }
-        if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1) * gridDim.x);
+        if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1));
     }
     // due_count is warp-uniform (every lane added the same ballot counts)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
@@ -369,6 +366,13 @@ __global__ void chunk_bounds_kernel(const int64_t* __restrict__ indptr, int64_t 
         if (W(mid) < target) lo = mid + 1; else hi = mid;
     }
     bounds[b] = b == G ? n_chunks : lo;
+}
+
+__global__ void owner_kernel(const int64_t* __restrict__ indptr, int64_t n, uint8_t* __restrict__ owner)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) owner[e] = (uint8_t)(v & 255);
 }
 
 __global__ void edge_records_kernel(const int32_t* __restrict__ col, const float* __restrict__ val, int64_t nnz,
@@ -632,11 +636,14 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
         edge_records_kernel<<<ceil_div(nnz, 256), 256, 0, s>>>(col, val, nnz, wmax.as<float>(), edges.as<int2>());
         UMAP_LAUNCH_CHECK("edge_records_kernel");
     }
+    Scratch owner;
+    UMAP_TRY(owner.alloc((size_t)std::max<int64_t>(nnz, 1), s));
+    owner_kernel<<<ceil_div(n, 256), 256, 0, s>>>(indptr, n, owner.as<uint8_t>());
+    UMAP_LAUNCH_CHECK("owner_kernel");
     UMAP_TRY(counter.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), s));
-    const size_t bar_words = 2;
-    UMAP_TRY(bar.alloc(bar_words * sizeof(unsigned int), s));
-    UMAP_CUDA_TRY(cudaMemsetAsync(bar.p, 0, bar_words * sizeof(unsigned int), s));
+    UMAP_TRY(bar.alloc(BAR_WORDS * sizeof(unsigned int), s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(bar.p, 0, BAR_WORDS * sizeof(unsigned int), s));
     const bool det = p->sgd_mode == UMAP_SGD_DETERMINISTIC;
     if (det) {
         UMAP_TRY(other.alloc(sizeof(float) * (size_t)n * dim, s));
@@ -649,6 +656,7 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
     A.key0 = (uint32_t)p->seed; A.key1 = (uint32_t)(p->seed >> 32);
     A.positives = counter.as<unsigned long long>();
     A.bar = bar.as<unsigned int>();
+    A.owner = owner.as<uint8_t>();
     {
         const char* dbg = getenv("UMAP_SGD_DEBUG");
         A.debug = dbg ? atoi(dbg) : 0;
