@@ -212,10 +212,13 @@ UMAP_API umap_status umap_transform_optimize(const int32_t* idx, const float* w,
 
 /* a10 input-space rank penalties for rows [row_begin, row_end) (R16): emb_idx is the
  * embedding kNN of those rows (n_rows x k, global ids).  knn_mode as in
- * umap_trustworthiness.  row_pen: n_rows int64 (optional NULL); *penalty (host) = sum. */
+ * umap_trustworthiness.  Y (optional, device, n x d_emb; NULL to omit) is the embedding:
+ * with d_emb == 2 the tensor-core path visits rows and columns in the Morton order of Y
+ * (a layout choice only: the integer result is the same).  row_pen: n_rows int64
+ * (optional NULL); *penalty (host) = sum. */
 UMAP_API umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
-                               int64_t row_begin, int64_t row_end, int32_t knn_mode, int64_t* row_pen,
-                               int64_t* penalty, void* stream);
+                               int64_t row_begin, int64_t row_end, int32_t knn_mode, const float* Y,
+                               int32_t d_emb, int64_t* row_pen, int64_t* penalty, void* stream);
 
 UMAP_API const char* umap_status_string(umap_status s);
 UMAP_API const char* umap_last_error(void);

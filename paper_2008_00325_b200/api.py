@@ -215,16 +215,21 @@ def transform_optimize(idx, w, Y_train, Yq, n_epochs_t, e_begin=1, e_end=None, q
     return Yq
 
 
-def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None, knn_mode="exact"):
+def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None, knn_mode="exact", Y=None):
+    """umap_trust_penalty: integer rank penalty of rows [row_begin, row_end).  Y (optional,
+    the n x 2 embedding) lets the tensor path visit rows in cluster order (same result)."""
     X = _dev(X, torch.float32, "X")
     emb_idx = _dev(emb_idx, torch.int32, "emb_idx")
+    if Y is not None:
+        Y = _dev(Y, torch.float32, "Y")
     n = X.shape[0]
     if row_end is None:
         row_end = n
     pen = torch.empty(row_end - row_begin, dtype=torch.int64, device=X.device)
     S = ctypes.c_int64()
     check(_lib.load().umap_trust_penalty(_ptr(X), n, X.shape[1], _ptr(emb_idx), k, row_begin, row_end,
-                                         KNN_MODES[knn_mode], _ptr(pen),
+                                         KNN_MODES[knn_mode], _ptr(Y), Y.shape[1] if Y is not None else 0,
+                                         _ptr(pen),
                                          ctypes.byref(S), _stream(X.device)), "umap_trust_penalty")
     return S.value, pen
 

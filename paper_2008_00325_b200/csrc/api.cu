@@ -32,7 +32,8 @@ umap_status transform_optimize(const int32_t* idx, const float* w, int64_t nq, i
                                float* Yq, const umap_params* p, int n_epochs_t, int e_begin, int e_end,
                                int64_t q_offset, int init, cudaStream_t s);
 umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
-                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, cudaStream_t s);
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, const float* Y,
+                          int d_emb, cudaStream_t s);
 bool dim_supported(int dim);
 int64_t last_rank_ambiguous();
 
@@ -524,8 +525,8 @@ umap_status umap_transform_optimize(const int32_t* idx, const float* w, int64_t 
 }
 
 umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
-                               int64_t row_begin, int64_t row_end, int32_t knn_mode, int64_t* row_pen,
-                               int64_t* penalty, void* stream)
+                               int64_t row_begin, int64_t row_end, int32_t knn_mode, const float* Y, int32_t d_emb,
+                               int64_t* row_pen, int64_t* penalty, void* stream)
 {
     UMAP_TRY(require_cuda());
     cudaStream_t s = (cudaStream_t)stream;
@@ -536,7 +537,8 @@ umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32
     UMAP_TRY(require_device(X, "X"));
     UMAP_TRY(require_device(emb_idx, "emb_idx"));
     UMAP_TRY(require_device(row_pen, "row_pen"));
-    UMAP_TRY(trust_penalty(X, n, d, emb_idx, k, row_begin, row_end, row_pen, penalty, knn_mode, s));
+    UMAP_TRY(require_device(Y, "Y"));
+    UMAP_TRY(trust_penalty(X, n, d, emb_idx, k, row_begin, row_end, row_pen, penalty, knn_mode, Y, d_emb, s));
     return UMAP_OK;
 }
 
@@ -747,7 +749,7 @@ umap_status trust_device(const float* Xd, int d, const float* Yd, int d_emb, int
         UMAP_TRY(run_knn(&pe, Yd, n, Yd, n, d_emb, k, 0, 1, 0, 1, eidx.as<int32_t>(), edist.as<float>(), s));
     }
     int64_t S = 0;
-    UMAP_TRY(trust_penalty(Xd, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, s));
+    UMAP_TRY(trust_penalty(Xd, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, Yd, d_emb, s));
     const double nn = (double)n, kk = (double)k;
     *T = 1.0 - (2.0 / (nn * kk * (2.0 * nn - 3.0 * kk - 1.0))) * (double)S;
     if (penalty) *penalty = S;

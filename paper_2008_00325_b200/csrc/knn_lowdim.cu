@@ -197,3 +197,73 @@ umap_status knn_grid2d(const float* Y, int64_t n, int k, int out_squared, int32_
 }
 
 }  // namespace umapb200
+
+// ---------------------------------------------------------------- cluster order of an embedding
+// Morton (Z-order) key of each 2-D point on a 2^16 x 2^16 grid over the bounding box, then a
+// stable radix sort of (key, row): perm[p] = the row at position p.  Used by the trust path
+// to visit rows and columns cluster by cluster (a layout choice; results do not depend on it).
+#include <cub/device/device_radix_sort.cuh>
+
+namespace umapb200 {
+namespace {
+
+__device__ __forceinline__ uint32_t spread16(uint32_t v)
+{
+    v &= 0xFFFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__global__ void morton_kernel(const float* __restrict__ Y, int64_t n, const float* __restrict__ box,
+                              uint32_t* __restrict__ keys, int32_t* __restrict__ vals)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const Grid g = grid_of(box, 65536);
+    const float2 p = reinterpret_cast<const float2*>(Y)[i];
+    const uint32_t cx = (uint32_t)cell_coord(p.x, g.x0, g.inv_h, 65536);
+    const uint32_t cy = (uint32_t)cell_coord(p.y, g.y0, g.inv_h, 65536);
+    keys[i] = spread16(cx) | (spread16(cy) << 1);
+    vals[i] = (int32_t)i;
+}
+
+}  // namespace
+
+// in place: sort (keys, vals) by key, stable (LSD radix)
+umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_t s)
+{
+    if (n <= 1) return UMAP_OK;
+    Scratch k2, v2, tmp;
+    UMAP_TRY(k2.alloc(sizeof(uint32_t) * (size_t)n, s));
+    UMAP_TRY(v2.alloc(sizeof(int32_t) * (size_t)n, s));
+    size_t bytes = 0;
+    UMAP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, k2.as<uint32_t>(), vals, v2.as<int32_t>(),
+                                                  (int)n, 0, 32, s));
+    UMAP_TRY(tmp.alloc(bytes, s));
+    UMAP_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys, k2.as<uint32_t>(), vals, v2.as<int32_t>(),
+                                                  (int)n, 0, 32, s));
+    count_launch(4);
+    UMAP_CUDA_TRY(cudaMemcpyAsync(keys, k2.p, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    UMAP_CUDA_TRY(cudaMemcpyAsync(vals, v2.p, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    return UMAP_OK;
+}
+
+umap_status cluster_order(const float* Y, int64_t n, int d_emb, int32_t* perm, cudaStream_t s)
+{
+    if (d_emb != 2) { set_last_error("cluster_order: 2-D embedding required"); return UMAP_ERR_UNSUPPORTED; }
+    Scratch box, keys;
+    UMAP_TRY(box.alloc(4 * sizeof(float), s));
+    int h_init[4] = {0x7f7fffff, 0x7f7fffff, (int)(0xff7fffffu ^ 0x7fffffffu), (int)(0xff7fffffu ^ 0x7fffffffu)};
+    UMAP_CUDA_TRY(cudaMemcpyAsync(box.p, h_init, sizeof(h_init), cudaMemcpyHostToDevice, s));
+    bbox_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4LL * num_sms()), 256, 0, s>>>(Y, n, box.as<float>());
+    UMAP_LAUNCH_CHECK("bbox_kernel");
+    UMAP_TRY(keys.alloc(sizeof(uint32_t) * (size_t)n, s));
+    morton_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Y, n, box.as<float>(), keys.as<uint32_t>(), perm);
+    UMAP_LAUNCH_CHECK("morton_kernel");
+    return sort_pairs_u32(keys.as<uint32_t>(), perm, n, s);
+}
+
+}  // namespace umapb200

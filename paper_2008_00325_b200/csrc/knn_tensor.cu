@@ -228,6 +228,7 @@ struct TcArgs {
     int32_t* amb;           // per (query row, column half) lists of reference rows to re-check
     int amb_cap;            // capacity per list
     int* amb_count;         // [n_q][2] entries per list (may exceed cap -> overflow)
+    const int32_t* self_col;  // RANK mode, optional: reference column of query q's own row
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
@@ -382,7 +383,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const int64_t q = q0 + row;
         const bool valid = q < a.nq;
         const float qn = valid ? a.qnorm[q] : 0.0f;
-        const int64_t self_j = (valid && a.exclude_self) ? q + a.self_shift : -1;
+        const int64_t self_j = (valid && a.exclude_self) ? (a.self_col ? (int64_t)a.self_col[q] : q + a.self_shift) : -1;
         const int k = a.k;
         float thr[TC_KT];
 #pragma unroll
@@ -643,17 +644,19 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
 // relative); norms are the fp32 sums of x_c^2.
 __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
                                   const double* __restrict__ colsum, double inv_n,
-                                  __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms)
+                                  __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms,
+                                  const int32_t* __restrict__ rowmap)
 {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
+    const int64_t src = rowmap ? (int64_t)rowmap[row] : row;  // output row `row` holds input row `src`
     float acc = 0.0f;
     __nv_bfloat16* o = Xs + row * (int64_t)(2 * d_pad);
     for (int f = lane; f < d_pad; f += 32) {
         __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
         if (f < d) {
-            const float c = X[row * d + f] - (float)(colsum[f] * inv_n);
+            const float c = X[src * d + f] - (float)(colsum[f] * inv_n);
             hi = __float2bfloat16_rn(c);
             lo = __float2bfloat16_rn(c - __bfloat162float(hi));
             acc = fmaf(c, c, acc);
@@ -685,7 +688,8 @@ __global__ void __launch_bounds__(32 * RF_WARPS)
 rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
                 const int32_t* __restrict__ amb, const int* __restrict__ amb_count, int cap_row,
                 const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
-                int64_t index_offset, int32_t* __restrict__ hist)
+                int64_t index_offset, int32_t* __restrict__ hist, const int32_t* __restrict__ qrow,
+                const int32_t* __restrict__ colmap)
 {
     __shared__ int h[RF_WARPS][16];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -693,7 +697,7 @@ rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int 
     if (q >= nq) return;
     if (lane < 16) h[warp][lane] = 0;
     __syncwarp();
-    const float* x = Xq + q * (int64_t)d;
+    const float* x = Xq + (qrow ? (int64_t)qrow[q] : q) * (int64_t)d;  // qrow: query q is input row qrow[q]
     float td[16];
     int32_t ti[16];
 #pragma unroll
@@ -705,7 +709,7 @@ rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int 
         const int cnt = min(amb_count[q * 2 + hf], cap_row);
         const int32_t* list = amb + (q * 2 + hf) * (int64_t)cap_row;
         for (int e = lane; e < cnt; e += 32) {
-            const int32_t l = list[e];
+            const int32_t l = colmap ? colmap[list[e]] : list[e];  // colmap: column -> input row
             const float v = exact_d2(x, Xr + (int64_t)l * d, d);
             const int32_t gid = (int32_t)(l + index_offset);
             int b = 0;
@@ -962,8 +966,67 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
 // non-cumulative bucket counts out (hist [rows][k]); the approximate pass only decides
 // pairs whose bucket is certain under the error bound, the rest are re-checked exactly.
 // *overflow != 0 tells the caller to fall back to the exact SIMT kernel.
+namespace {
+
+__global__ void order_maps_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ pos_of)
+{
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) pos_of[perm[p]] = (int32_t)p;
+}
+
+// queries of a row shard in cluster order: qrow[i] = input row, selfc[i] = its column, and the
+// shard's thresholds gathered into that order
+__global__ void shard_order_kernel(const int32_t* __restrict__ qperm, int64_t rows, int64_t row_begin,
+                                   const int32_t* __restrict__ pos_of, int k, const float* __restrict__ thr_d2,
+                                   const int32_t* __restrict__ thr_id, int32_t* __restrict__ qrow,
+                                   int32_t* __restrict__ selfc, float* __restrict__ thr_p, int32_t* __restrict__ thri_p)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int64_t r = qperm[i];
+    qrow[i] = (int32_t)(row_begin + r);
+    selfc[i] = pos_of[row_begin + r];
+    for (int t = 0; t < k; ++t) {
+        thr_p[i * k + t] = thr_d2[r * k + t];
+        thri_p[i * k + t] = thr_id[r * k + t];
+    }
+}
+
+__global__ void shard_keys_kernel(const int32_t* __restrict__ pos_of, int64_t row_begin, int64_t rows,
+                                  uint32_t* __restrict__ keys, int32_t* __restrict__ vals)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    keys[r] = (uint32_t)pos_of[row_begin + r];
+    vals[r] = (int32_t)r;
+}
+
+__global__ void unscatter_hist_kernel(const int32_t* __restrict__ qperm, int64_t rows, int k,
+                                      const int32_t* __restrict__ hist_p, int32_t* __restrict__ hist)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int64_t r = qperm[i];
+    for (int t = 0; t < k; ++t) hist[r * k + t] = hist_p[i * k + t];
+}
+
+}  // namespace
+
+umap_status cluster_order(const float* Y, int64_t n, int d_emb, int32_t* perm, cudaStream_t s);
+umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_t s);
+
+// Input-space rank counts of trustworthiness with the tensor-core GEMM (R16): queries =
+// rows [row_begin, row_end) of X, references = all of X.  Exact thresholds in, exact
+// non-cumulative bucket counts out (hist [rows][k]); the approximate pass only decides
+// pairs whose bucket is certain under the error bound, the rest are re-checked exactly.
+// Y (optional, n x 2): the embedding; rows and columns are then processed in the Morton
+// order of Y (counts do not depend on the order), which groups each query block with the
+// reference tiles of its own cluster: most column chunks then hold no candidate for any
+// row of a warp, and the others hold candidates for all of them.
+// *overflow != 0 tells the caller to fall back to the exact SIMT kernel.
 umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
-                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow, cudaStream_t s)
+                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow,
+                          const float* Y, int d_emb, cudaStream_t s)
 {
     *overflow = 0;
     if (rows == 0) return UMAP_OK;
@@ -971,6 +1034,31 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
     const int dk = 2 * d_pad;
     Scratch colsum, xr, rn, xq, qn, amb, ambc;
+    Scratch perm, pos_of, keys, qperm, qrow, selfc, thr_p, thri_p, hist_p;
+    const bool ordered = Y != nullptr && d_emb == 2 && n < (int64_t)INT32_MAX;
+    if (ordered) {
+        UMAP_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
+        UMAP_TRY(pos_of.alloc(sizeof(int32_t) * (size_t)n, s));
+        UMAP_TRY(cluster_order(Y, n, d_emb, perm.as<int32_t>(), s));
+        order_maps_kernel<<<ceil_div(n, 256), 256, 0, s>>>(perm.as<int32_t>(), n, pos_of.as<int32_t>());
+        UMAP_LAUNCH_CHECK("order_maps_kernel");
+        UMAP_TRY(keys.alloc(sizeof(uint32_t) * (size_t)rows, s));
+        UMAP_TRY(qperm.alloc(sizeof(int32_t) * (size_t)rows, s));
+        shard_keys_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(pos_of.as<int32_t>(), row_begin, rows,
+                                                              keys.as<uint32_t>(), qperm.as<int32_t>());
+        UMAP_LAUNCH_CHECK("shard_keys_kernel");
+        UMAP_TRY(sort_pairs_u32(keys.as<uint32_t>(), qperm.as<int32_t>(), rows, s));
+        UMAP_TRY(qrow.alloc(sizeof(int32_t) * (size_t)rows, s));
+        UMAP_TRY(selfc.alloc(sizeof(int32_t) * (size_t)rows, s));
+        UMAP_TRY(thr_p.alloc(sizeof(float) * (size_t)rows * k, s));
+        UMAP_TRY(thri_p.alloc(sizeof(int32_t) * (size_t)rows * k, s));
+        UMAP_TRY(hist_p.alloc(sizeof(int32_t) * (size_t)rows * k, s));
+        shard_order_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qperm.as<int32_t>(), rows, row_begin,
+                                                               pos_of.as<int32_t>(), k, thr_d2, thr_id,
+                                                               qrow.as<int32_t>(), selfc.as<int32_t>(),
+                                                               thr_p.as<float>(), thri_p.as<int32_t>());
+        UMAP_LAUNCH_CHECK("shard_order_kernel");
+    }
     UMAP_TRY(colsum.alloc(sizeof(double) * d, s));
     UMAP_CUDA_TRY(cudaMemsetAsync(colsum.p, 0, sizeof(double) * d, s));
     {
@@ -981,13 +1069,15 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(xr.alloc(sizeof(__nv_bfloat16) * (size_t)n * dk, s));
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)n, s));
     split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n,
-                                                          xr.as<__nv_bfloat16>(), rn.as<float>());
+                                                          xr.as<__nv_bfloat16>(), rn.as<float>(),
+                                                          ordered ? perm.as<int32_t>() : nullptr);
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
-    split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X + row_begin * (int64_t)d, rows, d, d_pad,
-                                                             colsum.as<double>(), 1.0 / (double)n,
-                                                             xq.as<__nv_bfloat16>(), qn.as<float>());
+    split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(ordered ? X : X + row_begin * (int64_t)d, rows, d,
+                                                             d_pad, colsum.as<double>(), 1.0 / (double)n,
+                                                             xq.as<__nv_bfloat16>(), qn.as<float>(),
+                                                             ordered ? qrow.as<int32_t>() : nullptr);
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
@@ -996,19 +1086,29 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     const int cap = 2048;
     UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * 2 * cap, s));
     UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * 2, s));
+    const float* thr_use = ordered ? thr_p.as<float>() : thr_d2;
+    const int32_t* thri_use = ordered ? thri_p.as<int32_t>() : thr_id;
+    int32_t* hist_use = ordered ? hist_p.as<int32_t>() : hist;
     TcArgs a{};
     a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = d_pad / TC_BK; a.kc = 0;
     a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
-    a.thr_d2 = thr_d2; a.k = k; a.margin = 5e-4f;
+    a.self_col = ordered ? selfc.as<int32_t>() : nullptr;
+    a.thr_d2 = thr_use; a.k = k; a.margin = 5e-4f;
     if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
-    a.hist = hist; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
+    a.hist = hist_use; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     a.amb_count = ambc.as<int>();
     UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
-    ProfScope ps(PROF_RANK_FIX, s);
-    rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(),
-                                                      ambc.as<int>(), cap, thr_d2, thr_id, k, 0, hist);
-    UMAP_LAUNCH_CHECK("rank_fix_kernel");
+        ProfScope ps(PROF_RANK_FIX, s);
+        rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(
+            ordered ? X : X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(), ambc.as<int>(), cap, thr_use,
+            thri_use, k, 0, hist_use, ordered ? qrow.as<int32_t>() : nullptr, ordered ? perm.as<int32_t>() : nullptr);
+        UMAP_LAUNCH_CHECK("rank_fix_kernel");
+    }
+    if (ordered) {
+        unscatter_hist_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qperm.as<int32_t>(), rows, k, hist_p.as<int32_t>(),
+                                                                  hist);
+        UMAP_LAUNCH_CHECK("unscatter_hist_kernel");
     }
     std::vector<int> counts((size_t)rows * 2);
     UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * 2, cudaMemcpyDeviceToHost, s));

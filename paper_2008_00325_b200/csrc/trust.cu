@@ -15,7 +15,8 @@ umap_status rank_count_exact(const float* Xq, int64_t nq, const float* X, int64_
                              Scratch& tmp, int* n_splits_out, cudaStream_t s);
 
 umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
-                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow, cudaStream_t s);
+                          const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow,
+                          const float* Y, int d_emb, cudaStream_t s);
 
 namespace {
 
@@ -88,7 +89,8 @@ __global__ void penalty_kernel(const int32_t* __restrict__ cnt, int n_splits, in
 }  // namespace
 
 umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_idx, int k, int64_t row_begin,
-                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, cudaStream_t s)
+                          int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, const float* Y,
+                          int d_emb, cudaStream_t s)
 {
     const int64_t rows = row_end - row_begin;
     if (rows <= 0) { if (penalty_host) *penalty_host = 0; return UMAP_OK; }
@@ -112,7 +114,7 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
     int overflow = 1;
     if (knn_mode == UMAP_KNN_TENSOR_BF16)
         UMAP_TRY(rank_count_tc(X, n, d, row_begin, rows, k, thr_d.as<float>(), thr_i.as<int32_t>(), cnt.as<int32_t>(),
-                               &overflow, s));
+                               &overflow, Y, d_emb, s));
     if (overflow)  // exact mode, or the tensor pass could not certify enough pairs
         UMAP_TRY(rank_count_exact(X + row_begin * (int64_t)d, rows, X, n, d, k, row_begin, thr_d.as<float>(),
                                   thr_i.as<int32_t>(), cnt.as<int32_t>(), tmp, &n_splits, s));

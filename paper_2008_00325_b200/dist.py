@@ -66,13 +66,14 @@ def sharded_knn(X, k, group=None, knn_fn=None, merge_fn=None):
     return merge_fn(torch.stack(gi), torch.stack(gd), k)
 
 
-def sharded_trust_penalty(X, emb_idx, k, group=None, penalty_fn=None, knn_mode="exact"):
-    """Integer trust penalty S with rows sharded; one all-reduce.  emb_idx: n x k embedding kNN."""
+def sharded_trust_penalty(X, emb_idx, k, group=None, penalty_fn=None, knn_mode="exact", Y=None):
+    """Integer trust penalty S with rows sharded; one all-reduce.  emb_idx: n x k embedding kNN;
+    Y (optional) the embedding, a layout hint for the tensor path."""
     if penalty_fn is None:
         from . import api
 
         def penalty_fn(X, e, k, lo, hi):
-            return api.trust_penalty(X, e, k, lo, hi, knn_mode=knn_mode)
+            return api.trust_penalty(X, e, k, lo, hi, knn_mode=knn_mode, Y=Y)
     rank, world = _rank_world(group)
     n = X.shape[0]
     lo, hi = shard_range(n, rank, world)
@@ -88,7 +89,7 @@ def sharded_trustworthiness(X, Y, k, group=None, knn_fn=None, penalty_fn=None, k
     """T(k) with the input-space rank counts sharded by rows (R16)."""
     knn_fn = knn_fn or _default_knn()
     emb_idx, _ = knn_fn(Y, Y, k, exclude_self=True)
-    S = sharded_trust_penalty(X, emb_idx, k, group=group, penalty_fn=penalty_fn, knn_mode=knn_mode)
+    S = sharded_trust_penalty(X, emb_idx, k, group=group, penalty_fn=penalty_fn, knn_mode=knn_mode, Y=Y)
     n = X.shape[0]
     return 1.0 - (2.0 / (n * k * (2.0 * n - 3.0 * k - 1.0))) * S, S
 

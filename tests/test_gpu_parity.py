@@ -390,6 +390,9 @@ def test_trust_tensor_exact_penalty(O, n, d, k, kind, emb):
     emb_idx, _ = O.knn(Y, Y, k, self_offset=0)
     S2, pen = U.trust_penalty(cu(X), cu(emb_idx[17:300]), k, 17, 300, knn_mode="tensor")
     assert np.array_equal(np_(pen), pen_ref[17:300])
+    # the same shard visited in the Morton order of Y (layout hint): identical per-row penalties
+    S3, pen3 = U.trust_penalty(cu(X), cu(emb_idx[17:300]), k, 17, 300, knn_mode="tensor", Y=cu(Y))
+    assert np.array_equal(np_(pen3), pen_ref[17:300]) and S3 == S2
 
 
 def test_trust_identity_is_one():
@@ -412,3 +415,24 @@ def test_c2_full_size_sampled_knn_and_trust(O):
     for r in rows:
         ri, rd = O.knn(X[r:r + 1], X, 15, self_offset=int(r))
         assert np.array_equal(gi[r], ri[0]) and np.array_equal(gd[r], rd[0])
+
+
+@pytest.mark.slow
+def test_c2_full_size_trust_tensor_equals_exact(O):
+    """C2 at full size in bench.py's launch configuration (umap_fit with trust_k = 15, tensor
+    mode, Morton-ordered rank counting): the integer penalty S equals the exact-mode S (fp32
+    SIMT ranks, pinned to the oracle at small sizes), and sampled rows' penalties equal the
+    oracle's, recomputed one row at a time."""
+    X = synth.make("C2")
+    Xg = cu(X)
+    Y, st = U.fit(Xg, n_neighbors=15, n_epochs=500, seed=0, knn_mode="tensor", trust_k=15)
+    T_exact, S_exact = U.trustworthiness(Xg, Y, 15, knn_mode="exact")
+    assert st["trust_penalty"] == S_exact and st["trustworthiness"] == T_exact
+    Yh = np_(Y)
+    emb_idx, _ = U.knn(Y, Y, 15, exclude_self=True)
+    rng = np.random.default_rng(1)
+    for r in np.concatenate([[0, 69999], rng.choice(70000, 4, replace=False)]):
+        r = int(r)
+        S_r, pen_r = U.trust_penalty(Xg, emb_idx[r:r + 1].contiguous(), 15, r, r + 1, knn_mode="tensor", Y=Y)
+        S_o, _ = O.trust_penalty(X, Yh, 15, r, r + 1)
+        assert S_r == S_o, r
