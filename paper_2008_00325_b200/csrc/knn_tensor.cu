@@ -20,6 +20,7 @@
 //     Whenever the candidate set holds the true k nearest the output equals the exact
 //     mode bit for bit.
 #include <cuda.h>
+#include <cmath>
 #include <cstdlib>
 #include <vector>
 #include <cuda_bf16.h>
@@ -229,9 +230,28 @@ struct TcArgs {
     int amb_cap;            // capacity per list
     int* amb_count;         // [n_q][2] entries per list (may exceed cap -> overflow)
     const int32_t* self_col;  // RANK mode, optional: reference column of query q's own row
+    int dense_min;            // RANK mode: see TC_DENSE_MIN
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
+
+// #{m : t[m] <= x} for ascending t[0..15] in registers: branch-free binary search over
+// t[0..14] (selects instead of dynamic register indexing), then t[15].
+__device__ __forceinline__ int cnt_le16(float x, const float (&t)[TC_KT])
+{
+    int i = (t[7] <= x) ? 8 : 0;
+    const float p1 = (i & 8) ? t[11] : t[3];
+    i += (p1 <= x) ? 4 : 0;
+    const float p2 = (i & 8) ? ((i & 4) ? t[13] : t[9]) : ((i & 4) ? t[5] : t[1]);
+    i += (p2 <= x) ? 2 : 0;
+    const float q0 = (i & 2) ? t[2] : t[0], q1 = (i & 2) ? t[6] : t[4];
+    const float q2 = (i & 2) ? t[10] : t[8], q3 = (i & 2) ? t[14] : t[12];
+    const float p3 = (i & 8) ? ((i & 4) ? q3 : q2) : ((i & 4) ? q1 : q0);
+    i += (p3 <= x) ? 1 : 0;
+    return i + ((t[15] <= x) ? 1 : 0);
+}
+constexpr int TC_DENSE_MIN = 16;  // a warp whose busiest lane has this many candidates in a chunk
+                                  // buckets all 32 columns branch-free instead of one by one
 
 // CG = 1: one CTA, MMA M = 128.  CG = 2: a CTA pair (cluster of 2 along the query blocks)
 // runs tcgen05.mma.cta_group::2 with M = 256: each CTA loads its own 128 query rows and
@@ -407,7 +427,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int64_t rb = r_lo + (int64_t)t * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
-            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2); c += 32) {
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
@@ -422,6 +442,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 }
                 if (!valid) cm = 0;
                 if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
+                if (__reduce_max_sync(0xffffffffu, (unsigned)__popc(cm)) >= (unsigned)a.dense_min) {
+                    // dense chunk (the row's own cluster): every column bucketed, updates predicated
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        const float rn = __shfl_sync(0xffffffffu, rn_l, u);
+                        const float E = c_m * (qn + rn);
+                        const int b_lo = cnt_le16(v[u] - E, thr), b_hi = cnt_le16(v[u] + E, thr);
+                        const bool act = (cm >> u) & 1u;
+                        if (act && b_hi == b_lo && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
+                        if (act && b_hi != b_lo) {
+                            if (n_amb < a.amb_cap) amb_row[n_amb] = (int32_t)(jb + u);
+                            ++n_amb;
+                        }
+                    }
+                    cm = 0;
+                }
                 while (__any_sync(0xffffffffu, cm != 0)) {
                     const int u = cm ? __ffs(cm) - 1 : 0;
                     const bool has = cm != 0;
@@ -439,12 +475,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const float rn = __shfl_sync(0xffffffffu, rn_l, u);
                     const float E = c_m * (qn + rn);
                     const float hiv = d2a + E, lov = d2a - E;
-                    int b_hi = 0, b_lo = 0;  // #thresholds <= d2~ + E, <= d2~ - E
-#pragma unroll
-                    for (int tt = 0; tt < TC_KT; ++tt) {
-                        b_hi += thr[tt] <= hiv;
-                        b_lo += thr[tt] <= lov;
-                    }
+                    const int b_hi = cnt_le16(hiv, thr), b_lo = cnt_le16(lov, thr);  // #thresholds <= d2~ +- E
                     const bool amb = has && b_hi != b_lo;
                     if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
                     if (amb) {
@@ -1093,9 +1124,22 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     a.qnorm = qn.as<float>(); a.rnorm = rn.as<float>(); a.nq = rows; a.nr = n; a.kblocks = d_pad / TC_BK; a.kc = 0;
     a.split_len = (n + TC_BN - 1) / TC_BN * TC_BN; a.self_shift = row_begin; a.exclude_self = 1; a.index_offset = 0;
     a.self_col = ordered ? selfc.as<int32_t>() : nullptr;
-    a.thr_d2 = thr_use; a.k = k; a.margin = 5e-4f;
+    // certification margin c: |d2~ - R2(q, r)| <= c (|q|^2 + |r|^2) under any
+    // accumulation order with round-to-nearest or truncating fp32 adds (u = 2^-24):
+    // split representation + accumulation of 3 d_pad products + norms + R2's own error + final ops,
+    // times 1.1 (C2: 2.94e-4)
+    {
+        const double u = std::ldexp(1.0, -24);
+        const double c = 3.0 * std::ldexp(1.0, -16) * 0.5 + 3.0 * d_pad * 2.0 * u * 0.5 +
+                         ((d + 31) / 32 + 5) * u + (d + 1.0) * u * 2.0 + 2.0 * u;
+        a.margin = (float)(1.1 * c);
+    }
+    a.thr_d2 = thr_use; a.k = k;
     if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
     a.hist = hist_use; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
+    if (const char* dbg = getenv("UMAP_TC_DEBUG")) a.debug = atoi(dbg);  // profiling only (results invalid)
+    a.dense_min = TC_DENSE_MIN;
+    if (const char* dm = getenv("UMAP_TC_DENSE_MIN")) a.dense_min = atoi(dm);  // tuning knob
     a.amb_count = ambc.as<int>();
     UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
