@@ -529,14 +529,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
-                const float rn_l = (jb + lane < r_hi) ? __ldg(a.rnorm + jb + lane) : INFINITY;
+                // the accumulator holds -d2/2 (norms folded into the GEMM); out-of-range
+                // columns (zero-filled TMA rows) are masked by their index
+                const float nthr = -0.5f * thr;
+                const int valid_cols = (int)imin64(32, r_hi - jb);
                 uint32_t cm = 0;  // columns of this chunk that beat the running threshold
 #pragma unroll
-                for (int u = 0; u < 32; ++u) {
-                    const float rn = __shfl_sync(0xffffffffu, rn_l, u);
-                    v[u] = fmaf(-2.0f, v[u], qn + rn);
-                    cm |= (uint32_t)(v[u] < thr) << u;
-                }
+                for (int u = 0; u < 32; ++u) cm |= (uint32_t)(v[u] > nthr) << u;
+                if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
                 if (!valid) cm = 0;
                 if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
                 // one insertion round per candidate of the busiest lane; each lane inserts its
@@ -554,7 +554,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     for (int i = 0; i < 4; ++i) w4[i] = (u & 4) ? w8[2 * i + 1] : w8[2 * i];
 #pragma unroll
                     for (int i = 0; i < 2; ++i) w2[i] = (u & 8) ? w4[2 * i + 1] : w4[2 * i];
-                    const float sel = (u & 16) ? w2[1] : w2[0];
+                    const float sel = -2.0f * ((u & 16) ? w2[1] : w2[0]);
                     float cv = (has && sel < thr) ? sel : INFINITY;
                     int32_t ci = (int32_t)(jb + u + a.index_offset);
 #pragma unroll
@@ -647,9 +647,13 @@ __global__ void colsum_kernel(const float* __restrict__ X, int64_t n, int d, dou
     }
 }
 
+// role 1 (query / A operand): padding columns d_pad-6 .. d_pad-1 = [n1, n2, n3, 1, 1, 1];
+// role 2 (reference / B operand): [1, 1, 1, n1, n2, n3], where n1 + n2 + n3 = -|x_c|^2 / 2 in
+// three BF16 pieces (24 significant bits).  The GEMM then accumulates
+// q.r - |q|^2/2 - |r|^2/2 = -d2/2 directly (norms folded into the padding of the last K slab).
 __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
                                    const double* __restrict__ colsum, double inv_n, __nv_bfloat16* __restrict__ Xc,
-                                   float* __restrict__ norms)
+                                   float* __restrict__ norms, int role)
 {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -667,6 +671,18 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
+    if (role && lane < 6) {
+        const float nh = -0.5f * acc;
+        const __nv_bfloat16 n1 = __float2bfloat16_rn(nh);
+        const float r1 = nh - __bfloat162float(n1);
+        const __nv_bfloat16 n2 = __float2bfloat16_rn(r1);
+        const __nv_bfloat16 n3 = __float2bfloat16_rn(r1 - __bfloat162float(n2));
+        const __nv_bfloat16 one = __float2bfloat16_rn(1.0f);
+        const int j = lane < 3 ? lane : lane - 3;
+        const __nv_bfloat16 piece = j == 0 ? n1 : (j == 1 ? n2 : n3);
+        const bool norm_slot = (role == 1) == (lane < 3);
+        Xc[row * d_pad + (d_pad - 6) + lane] = norm_slot ? piece : one;
+    }
 }
 
 // split-BF16 operands for the RANK mode: x_c = x - mean (fp32), hi = bf16(x_c),
@@ -843,10 +859,11 @@ umap_status make_map(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, in
 
 // centred BF16 copy + norms of X (rows n) with the given column mean (colsum / n_mean)
 umap_status prep_bf16(const float* X, int64_t n, int d, int d_pad, const double* colsum, int64_t n_mean,
-                      __nv_bfloat16* Xc, float* norms, cudaStream_t s)
+                      __nv_bfloat16* Xc, float* norms, int role, cudaStream_t s)
 {
     if (n == 0) return UMAP_OK;
-    center_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum, 1.0 / (double)n_mean, Xc, norms);
+    center_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum, 1.0 / (double)n_mean, Xc, norms,
+                                                             role);
     UMAP_LAUNCH_CHECK("center_bf16_kernel");
     return UMAP_OK;
 }
@@ -927,8 +944,7 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
         set_last_error("tensor kNN: row count exceeds the TMA coordinate range");
         return UMAP_ERR_INVALID_ARGUMENT;
     }
-    const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
-    const bool same = (Xq == Xr && nq == nr);
+    const int d_pad = (d + 6 + TC_BK - 1) / TC_BK * TC_BK;  // >= 6 padding columns for the folded norms
     Scratch colsum, xr16, rn, xq16, qn;
     UMAP_TRY(colsum.alloc(sizeof(double) * d, s));
     UMAP_CUDA_TRY(cudaMemsetAsync(colsum.p, 0, sizeof(double) * d, s));
@@ -939,16 +955,13 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     }
     UMAP_TRY(xr16.alloc(sizeof(__nv_bfloat16) * (size_t)nr * d_pad, s));
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)nr, s));
-    UMAP_TRY(prep_bf16(Xr, nr, d, d_pad, colsum.as<double>(), nr, xr16.as<__nv_bfloat16>(), rn.as<float>(), s));
-    const __nv_bfloat16* q16 = xr16.as<__nv_bfloat16>();
-    const float* qnp = rn.as<float>();
-    if (!same) {
-        UMAP_TRY(xq16.alloc(sizeof(__nv_bfloat16) * (size_t)nq * d_pad, s));
-        UMAP_TRY(qn.alloc(sizeof(float) * (size_t)nq, s));
-        UMAP_TRY(prep_bf16(Xq, nq, d, d_pad, colsum.as<double>(), nr, xq16.as<__nv_bfloat16>(), qn.as<float>(), s));
-        q16 = xq16.as<__nv_bfloat16>();
-        qnp = qn.as<float>();
-    }
+    UMAP_TRY(prep_bf16(Xr, nr, d, d_pad, colsum.as<double>(), nr, xr16.as<__nv_bfloat16>(), rn.as<float>(), 2, s));
+    // queries always get their own copy (A role; for a self-kNN the same rows in the other role)
+    UMAP_TRY(xq16.alloc(sizeof(__nv_bfloat16) * (size_t)nq * d_pad, s));
+    UMAP_TRY(qn.alloc(sizeof(float) * (size_t)nq, s));
+    UMAP_TRY(prep_bf16(Xq, nq, d, d_pad, colsum.as<double>(), nr, xq16.as<__nv_bfloat16>(), qn.as<float>(), 1, s));
+    const __nv_bfloat16* q16 = xq16.as<__nv_bfloat16>();
+    const float* qnp = qn.as<float>();
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, q16, nq, d_pad, TC_BM));
     UMAP_TRY(make_map(&map_r, xr16.as<__nv_bfloat16>(), nr, d_pad, TC_BN / tc_cg()));

@@ -10,8 +10,12 @@ timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_$
 timeout 600 python bench.py --sgd-mode hogwild --no-cpu-baseline --no-e2e > gpurun_out/bench_hog_${TAG}.json 2>> gpurun_out/bench_${TAG}.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'knn_tc|sgd_persistent|rerank|rank_fix|grid_knn|thresholds|smooth_knn|union_rows' \
-    -c 10 -o gpurun_out/prof_${TAG} -f python tools/profile_step.py --knn-mode tensor > gpurun_out/prof_${TAG}.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'knn_tc|sgd_persistent|rerank|rank_fix' \
+    -c 5 -o /tmp/prof_${TAG} -f python tools/profile_step.py --knn-mode tensor > gpurun_out/prof_${TAG}.log 2>&1
+ncu -i /tmp/prof_${TAG}.ncu-rep --page raw --csv > gpurun_out/prof_${TAG}_raw.csv 2>/dev/null
+ncu -i /tmp/prof_${TAG}.ncu-rep --page details > gpurun_out/prof_${TAG}_details.txt 2>/dev/null
+cp /tmp/prof_${TAG}.ncu-rep gpurun_out/ 2>/dev/null
+du -sh gpurun_out
 ls -la gpurun_out
-tail -3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log
+tail -n 3 gpurun_out/pytest_gpu_${TAG}.log gpurun_out/smoke_${TAG}.log
 cat gpurun_out/bench_${TAG}.json gpurun_out/bench_hog_${TAG}.json
