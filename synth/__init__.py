@@ -62,6 +62,67 @@ def lowrank(n: int, d: int, blobs: int = 10, seed: int = 0, rank: int = 10,
     return (X, lab) if return_labels else X
 
 
+def lowrank_model(d: int, blobs: int, seed: int, rank: int = 10):
+    """Blob centres C (B x d) and low-rank bases A (B x rank x d) of the lowrank recipe, from
+    their own PCG64 stream, so that several samples (train rows, transform chunks) share one
+    mixture: ``C = N(0,1)*3``, ``A = N(0,1)/sqrt(rank)``."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    C = g.standard_normal((blobs, d)) * 3.0
+    A = g.standard_normal((blobs, rank, d)) / np.sqrt(rank)
+    return C, A
+
+
+def lowrank_sample(model, n: int, seed: int, return_labels: bool = False):
+    """n rows from a ``lowrank_model``: ``lab = integers(0,B,n)``, ``Z = N(0,1)^{n x r}*2``,
+    ``E = N(0,1)^{n x d}*0.3``, ``X = C[lab] + Z A[lab] + E`` (fp32), drawn in that order."""
+    C, A = model
+    blobs, rank, d = A.shape
+    g = np.random.Generator(np.random.PCG64(seed))
+    lab = g.integers(0, blobs, n)
+    Z = g.standard_normal((n, rank)) * 2.0
+    E = g.standard_normal((n, d)).astype(np.float32) * np.float32(0.3)
+    X = C[lab].astype(np.float32) + E
+    for c in range(blobs):
+        sel = np.nonzero(lab == c)[0]
+        if sel.size:
+            X[sel] += (Z[sel] @ A[c]).astype(np.float32)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    return (X, lab) if return_labels else X
+
+
+def c5_train(n: int = 100000, d: int = 784, seed: int = 4):
+    """C5 training rows: the model of seed 4, sample seed 40."""
+    return lowrank_sample(lowrank_model(d, 10, seed), n, seed * 10)
+
+
+def c5_transform_chunk(chunk: int, rows: int = 1000000, d: int = 784, seed: int = 4):
+    """C5 transform rows, chunk by chunk (8 chunks of 1,000,000 = 8,000,000 rows): the same
+    mixture as ``c5_train``, sample seed 41 + chunk."""
+    return lowrank_sample(lowrank_model(d, 10, seed), rows, seed * 10 + 1 + chunk)
+
+
+def lowrank_sample_device(model, n: int, seed: int, device="cuda"):
+    """``lowrank_sample`` drawn on the GPU (torch Philox stream of ``seed``) for the 25 GB C5
+    transform set: the same mixture and recipe, a different random stream.  Rows used for
+    oracle checks are copied back, so both sides read the same bytes."""
+    import torch
+    C, A = model
+    blobs, rank, d = A.shape
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    lab = torch.randint(0, blobs, (n,), generator=g, device=device)
+    Z = torch.randn((n, rank), generator=g, device=device) * 2.0
+    X = torch.randn((n, d), generator=g, device=device) * 0.3
+    Ct = torch.as_tensor(C, dtype=torch.float32, device=device)
+    At = torch.as_tensor(A, dtype=torch.float32, device=device)
+    X += Ct[lab]
+    for c in range(blobs):
+        sel = torch.nonzero(lab == c).squeeze(1)
+        if sel.numel():
+            X[sel] += Z[sel] @ At[c]
+    return X.contiguous()
+
+
 def iso(n: int, d: int, blobs: int = 10, seed: int = 0, return_labels: bool = False):
     """Isotropic blobs (Table 4): centres U(-10,10)^d, unit noise."""
     g = np.random.Generator(np.random.PCG64(seed))

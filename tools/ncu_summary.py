@@ -12,10 +12,18 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", 
      "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
      "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct"]
 rep, out = sys.argv[1], sys.argv[2]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv") or rep.endswith(".csv.gz"):  # a raw-page CSV exported on the GPU box
+    import gzip
+    raw = (gzip.open(rep, "rt") if rep.endswith(".gz") else open(rep)).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
+units = dict(zip(h, rows[1]))
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1, "usecond": 1e3,
+         "msecond": 1e6, "second": 1e9, "sector": 1, "Ksector": 1e3, "Msector": 1e6, "Gsector": 1e9,
+         "inst": 1, "Kinst": 1e3, "Minst": 1e6, "Ginst": 1e9}
 res = {"source": rep, "kernels": {}}
 for r in rows[2:]:
     d = dict(zip(h, r))
@@ -24,7 +32,7 @@ for r in rows[2:]:
     for m in M:
         if m in d:
             try:
-                rec[m] = float(d[m].replace(",", ""))
+                rec[m] = float(d[m].replace(",", "")) * SCALE.get(units.get(m, ""), 1)
             except ValueError:
                 rec[m] = d[m]
     if "dram__bytes_read.sum" in rec:
