@@ -86,6 +86,28 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
         "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar)
         : "memory");
 }
+// TMA with an L2 eviction-priority policy (createpolicy): the CTA's own query tile is
+// re-read for every reference tile (evict_last keeps it), reference tiles stream through
+__device__ __forceinline__ uint64_t l2_policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                                 uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -155,11 +177,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
     }
 }
 // TMA load whose completion bytes go to the leader CTA's mbarrier (cluster address)
-__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster)
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster,
+                                                uint64_t pol)
 {
     asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        ::"r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar_cluster)
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(dst), "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar_cluster), "l"(pol)
         : "memory");
 }
 // instruction descriptor with M = 256 (pair), N = 256
@@ -319,6 +343,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             // MODE 1 (split operands, rows [hi | lo] of 2 KB columns): per K slab two stages,
             // the hi parts (A_hi, B_hi) then the lo parts (A_lo, B_lo)
             constexpr int PARTS = MODE == 1 ? 2 : 1;
+            // (profiling knob UMAP_TC_DEBUG bit 2: references evict_last too; bit 3: both evict_normal)
+            uint64_t pol_a = l2_policy_evict_last();
+            uint64_t pol_b = (a.debug & 4) ? l2_policy_evict_last() : l2_policy_evict_first();
+            if (a.debug & 8) {
+                asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_a));
+                pol_b = pol_a;
+            }
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
                 const int y_r = (int)(r_lo + (int64_t)t * TC_BN);
@@ -334,12 +365,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                             // both CTAs' bytes complete on the leader's full barrier
                             if (leader) mbar_expect_tx(full0 + 8 * s, CG * STAGE_C);
                             const uint32_t fb = mapa_shared(full0 + 8 * s, 0);
-                            tma_load_2d_cg2(dst, &map_q, x, (int)q0, fb);
-                            tma_load_2d_cg2(dst + A_BYTES, &map_r, x, y_r + (int)(rank * B_ROWS), fb);
+                            tma_load_2d_cg2(dst, &map_q, x, (int)q0, fb, pol_a);
+                            tma_load_2d_cg2(dst + A_BYTES, &map_r, x, y_r + (int)(rank * B_ROWS), fb, pol_b);
                         } else {
                             mbar_expect_tx(full0 + 8 * s, STAGE_C);
-                            tma_load_2d(dst, &map_q, x, (int)q0, full0 + 8 * s);
-                            tma_load_2d(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s);
+                            tma_load_2d_hint(dst, &map_q, x, (int)q0, full0 + 8 * s, pol_a);
+                            tma_load_2d_hint(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s, pol_b);
                         }
                     }
                 }
