@@ -800,6 +800,128 @@ rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int 
     if (lane < k) hist[q * k + lane] += h[warp][lane];
 }
 
+// The same re-check with the candidate rows staged by the TMA bulk-copy engine: per warp a
+// double-buffered smem ring of 33 row segments (32 candidates + the query row) of RB_CH
+// floats; lane p issues one cp.async.bulk for its candidate's segment, completion is counted
+// on the buffer's mbarrier, and each lane then continues the sequential R2 fmaf chain of its
+// pair from shared memory with 16-byte loads (row stride RB_CH = 100 words = 4 mod 32: the
+// eight lanes of each LDS.128 phase hit 32 distinct banks).  Requires d % 4 == 0 (16-byte
+// aligned rows); the value is bit-identical to exact_d2.  8 warps x 100-float segments
+// measured best at C2 (4.3 ms vs 7.2 ms for per-lane LDG streaming; 4 x 196: 4.9, 16 x 52: 4.9).
+constexpr int RB_WARPS = 8;
+constexpr int RB_CH = 100;
+constexpr size_t RB_WARP_FLOATS = 2 * 33 * RB_CH;
+constexpr size_t RB_SMEM = RB_WARPS * RB_WARP_FLOATS * sizeof(float) + RB_WARPS * 2 * sizeof(uint64_t);
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+// 32 pairs (x, Xr[l_lane]) (l < 0: none) through the warp's bulk ring; returns lane's R2 value.
+// ph: per-buffer phase bits of the ring's two mbarriers (updated).
+__device__ __forceinline__ float exact_d2_bulk(const float* __restrict__ x, const float* __restrict__ Xr,
+                                               int32_t l, int d, float* ring, uint32_t bar0, uint32_t& ph, int lane)
+{
+    const unsigned act = __ballot_sync(0xffffffffu, l >= 0);
+    const int nch = (d + RB_CH - 1) / RB_CH;
+    auto issue = [&](int c) {
+        const int b = c & 1;
+        const int w = min(RB_CH, d - c * RB_CH);
+        const uint32_t bytes = (uint32_t)w * 4u;
+        const uint32_t bar = bar0 + 8 * b;
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(ring + (size_t)b * 33 * RB_CH);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads vs the async refill
+        __syncwarp();
+        if (lane == 0) {
+            mbar_expect_tx(bar, bytes * (uint32_t)(__popc(act) + 1));
+            bulk_g2s(base + 32u * RB_CH * 4u, x + (size_t)c * RB_CH, bytes, bar);
+        }
+        __syncwarp();
+        if (l >= 0) bulk_g2s(base + (uint32_t)lane * RB_CH * 4u, Xr + (int64_t)l * d + (size_t)c * RB_CH, bytes, bar);
+    };
+    issue(0);
+    float s = 0.0f;
+    for (int c = 0; c < nch; ++c) {
+        const int b = c & 1;
+        if (c + 1 < nch) issue(c + 1);
+        mbar_wait(bar0 + 8 * b, (ph >> b) & 1u);
+        ph ^= 1u << b;
+        const float4* rr = reinterpret_cast<const float4*>(ring + (size_t)b * 33 * RB_CH + (size_t)lane * RB_CH);
+        const float4* xx = reinterpret_cast<const float4*>(ring + (size_t)b * 33 * RB_CH + 32 * RB_CH);
+        const int w4 = min(RB_CH, d - c * RB_CH) >> 2;
+        for (int j = 0; j < w4; ++j) {
+            const float4 a = xx[j], y = rr[j];
+            float t = __fsub_rn(a.x, y.x); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.y, y.y); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.z, y.z); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.w, y.w); s = __fmaf_rn(t, t, s);
+        }
+        __syncwarp();  // every lane is done with buffer b before it is refilled (iteration c + 1 issues c + 2)
+    }
+    return s;
+}
+
+__global__ void __launch_bounds__(32 * RB_WARPS, 1)
+rank_fix_bulk_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
+                     const int32_t* __restrict__ amb, const int* __restrict__ amb_count, int cap_row,
+                     const float* __restrict__ thr_d2, const int32_t* __restrict__ thr_id, int k,
+                     int64_t index_offset, int32_t* __restrict__ hist, const int32_t* __restrict__ qrow,
+                     const int32_t* __restrict__ colmap)
+{
+    extern __shared__ __align__(16) float rb_smem[];
+    __shared__ int h[RB_WARPS][16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* ring = rb_smem + (size_t)warp * RB_WARP_FLOATS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rb_smem + RB_WARPS * RB_WARP_FLOATS);
+    const uint32_t bar0 = smem_u32(bars + 2 * warp);
+    if (lane == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (lane < 16) h[warp][lane] = 0;
+    __syncwarp();
+    uint32_t ph = 0;
+    // persistent over query rows: warp w of block b takes rows b * RB_WARPS + w, + grid stride
+    for (int64_t q = (int64_t)blockIdx.x * RB_WARPS + warp; q < nq; q += (int64_t)gridDim.x * RB_WARPS) {
+        const float* x = Xq + (qrow ? (int64_t)qrow[q] : q) * (int64_t)d;
+        float td[16];
+        int32_t ti[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            td[t] = t < k ? thr_d2[q * k + t] : INFINITY;
+            ti[t] = t < k ? thr_id[q * k + t] : INT32_MAX;
+        }
+        const int c0 = min(amb_count[q * 2], cap_row), c1 = min(amb_count[q * 2 + 1], cap_row);
+        const int32_t* list0 = amb + (q * 2) * (int64_t)cap_row;
+        const int32_t* list1 = list0 + cap_row;
+        for (int base = 0; base < c0 + c1; base += 32) {
+            const int e = base + lane;
+            int32_t l = -1;
+            if (e < c0 + c1) {
+                const int32_t col = e < c0 ? list0[e] : list1[e - c0];
+                l = colmap ? colmap[col] : col;
+            }
+            const float v = exact_d2_bulk(x, Xr, l, d, ring, bar0, ph, lane);
+            if (l >= 0) {
+                const int32_t gid = (int32_t)(l + index_offset);
+                int b = 0;
+#pragma unroll
+                for (int t = 0; t < 16; ++t) b += (t < k) && !key_less(v, gid, td[t], ti[t]);
+                if (b < k) atomicAdd(&h[warp][b], 1);
+            }
+        }
+        __syncwarp();
+        if (lane < k) {
+            hist[q * k + lane] += h[warp][lane];
+            h[warp][lane] = 0;
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void rerank_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int d, int64_t nq,
                               const int32_t* __restrict__ cand, int kc, int64_t index_offset, int k, int out_squared,
                               int32_t* __restrict__ idx, float* __restrict__ dist)
@@ -1188,10 +1310,27 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
         ProfScope ps(PROF_RANK_FIX, s);
-        rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(
-            ordered ? X : X + row_begin * (int64_t)d, X, d, rows, amb.as<int32_t>(), ambc.as<int>(), cap, thr_use,
-            thri_use, k, 0, hist_use, ordered ? qrow.as<int32_t>() : nullptr, ordered ? perm.as<int32_t>() : nullptr);
-        UMAP_LAUNCH_CHECK("rank_fix_kernel");
+        const float* xq = ordered ? X : X + row_begin * (int64_t)d;
+        const int32_t* qmap = ordered ? qrow.as<int32_t>() : nullptr;
+        const int32_t* cmap = ordered ? perm.as<int32_t>() : nullptr;
+        if (d % 4 == 0 && !getenv("UMAP_RANKFIX_LDG")) {  // TMA bulk staging (16-byte aligned rows)
+            static bool cfg = false;
+            if (!cfg) {
+                UMAP_CUDA_TRY(cudaFuncSetAttribute(rank_fix_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)RB_SMEM));
+                cfg = true;
+            }
+            const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows, RB_WARPS), num_sms());
+            rank_fix_bulk_kernel<<<grid, 32 * RB_WARPS, RB_SMEM, s>>>(xq, X, d, rows, amb.as<int32_t>(),
+                                                                     ambc.as<int>(), cap, thr_use, thri_use, k, 0,
+                                                                     hist_use, qmap, cmap);
+            UMAP_LAUNCH_CHECK("rank_fix_bulk_kernel");
+        } else {
+            rank_fix_kernel<<<ceil_div(rows, RF_WARPS), 32 * RF_WARPS, 0, s>>>(xq, X, d, rows, amb.as<int32_t>(),
+                                                                              ambc.as<int>(), cap, thr_use, thri_use,
+                                                                              k, 0, hist_use, qmap, cmap);
+            UMAP_LAUNCH_CHECK("rank_fix_kernel");
+        }
     }
     if (ordered) {
         unscatter_hist_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qperm.as<int32_t>(), rows, k, hist_p.as<int32_t>(),
