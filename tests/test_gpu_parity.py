@@ -360,7 +360,7 @@ def test_transform_end_to_end_and_partition_invariance(O):
 
 
 # ------------------------------------------------------------------- trust (a10)
-@pytest.mark.parametrize("n,d,k", [(700, 20, 15), (1000, 64, 5), (300, 7, 1), (257, 3, 40)])
+@pytest.mark.parametrize("n,d,k", [(700, 20, 15), (1000, 64, 5), (300, 7, 1), (257, 3, 40), (900, 36, 24)])
 def test_trust_penalty_exact(O, n, d, k):
     X = synth.lowrank(n, d, seed=8)
     Y = synth.uniform_embedding(n, 2, seed=9)
