@@ -251,9 +251,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # UMAP_BENCH_ONE_GPU=1 (testing only): every rank on cuda:0 with gloo, to exercise the
+    # N > 1 code path on a single-GPU box; timings from such a run are not bench values
+    one_gpu = os.environ.get("UMAP_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = cfg_of(args.config)
     n, d, k, N = c["n"], c["d"], c["k"], c["n_epochs"]
     trust_k = 15
@@ -310,6 +318,25 @@ def run_ours(args):
     # ---- e2e through the public C ABI with HOST buffers: umap_fit(X host -> Y host, trust_k):
     # the library stages X host->device and Y device->host inside the call
     e2e = None
+    if not args.no_e2e and world > 1:
+        # N > 1: every rank stages the (replicated) pinned host X itself, runs the sharded step
+        # and reads its result back; wall clock between barriers, max over ranks
+        e2e_ms = []
+        for i in range(max(1, min(args.steps, 3))):
+            flush.fill_(float(i))
+            barrier()
+            t0 = time.perf_counter()
+            Xd = X_host.to("cuda", non_blocking=True)
+            Y, st_e, Te = step(Xd)
+            Yh = Y.to("cpu")
+            barrier()
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            del Xd
+        t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(t.item()) / 1e3, "unit": "s", "h2d_bytes_per_step": int(X_host.numel() * 4),
+               "d2h_bytes_per_step": int(Yh.numel() * 4), "api": "dist.sharded_fit + sharded_trustworthiness",
+               "timer": "host wall clock between barriers, max over ranks"}
     if not args.no_e2e and world == 1:
         e2e_ms = []
         Y_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)

@@ -99,7 +99,13 @@ def sharded_fit(X, group=None, knn_fn=None, merge_fn=None, fit_knn_fn=None, **kw
     if fit_knn_fn is None:
         from . import api
         fit_knn_fn = api.fit_knn
-    k = kw.get("n_neighbors", 15)
+    if knn_fn is None:
+        from . import api
+        mode = kw.get("knn_mode", "exact")
+
+        def knn_fn(Xq, Xr, k, **a):
+            return api.knn(Xq, Xr, k, mode=mode, **a)
+    k = kw.pop("n_neighbors", 15)  # fit_knn takes k from the graph's shape
     idx, dst = sharded_knn(X, k, group=group, knn_fn=knn_fn, merge_fn=merge_fn)
     return fit_knn_fn(idx, dst, **kw)
 

@@ -84,6 +84,17 @@ def _worker(rank, world, port, q):
         from paper_2008_00325_b200 import dist as D
         X = torch.from_numpy(synth.lowrank(130, 6, blobs=3, seed=1))
         idx, dd = D.sharded_knn(X, 7, knn_fn=knn_cpu, merge_fn=merge_cpu)
+        # sharded_fit as bench.py calls it at N > 1 (the fit keyword arguments pass through;
+        # the graph's k comes from the merged kNN)
+        seen = {}
+
+        def fit_knn_rec(i, d, **kw):
+            seen.update(kw, k=i.shape[1])
+            return i, d
+        fi, fd = D.sharded_fit(X, knn_fn=knn_cpu, merge_fn=merge_cpu, fit_knn_fn=fit_knn_rec, n_neighbors=7,
+                               n_epochs=5, seed=0, knn_mode="exact", sgd_mode="deterministic")
+        assert seen["k"] == 7 and "n_neighbors" not in seen and seen["n_epochs"] == 5
+        assert torch.equal(fi, idx) and torch.equal(fd, dd)
         Y = torch.from_numpy(synth.uniform_embedding(130, 2, seed=2))
         emb_idx, _ = knn_cpu(Y, Y, 5, exclude_self=True)
         S = D.sharded_trust_penalty(X, emb_idx, 5, penalty_fn=penalty_cpu)
