@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <vector>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -225,6 +226,12 @@ struct TcArgs {
     int* amb_count;         // [n_q][2] entries per list (may exceed cap -> overflow)
     const int32_t* self_col;  // RANK mode, optional: reference column of query q's own row
     int dense_min;            // RANK mode: see TC_DENSE_MIN
+    // RANK mode, optional: the 256-row query block b (= blockIdx.x / 2) visits only the reference
+    // tiles tile_list[b * tile_ld + 0 .. tile_count[b]) -- the tiles the coarse pass flagged
+    const int32_t* tile_list;
+    const int32_t* tile_count;
+    int tile_ld;
+    uint8_t* flags;           // MODE 2 (coarse pass): flags[b * tile_ld + t] = 1 if tile t may matter
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
@@ -271,7 +278,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     const int64_t q0 = (int64_t)blockIdx.x * TC_BM;
     const int64_t r_lo = (int64_t)blockIdx.y * a.split_len;
     const int64_t r_hi = imin64(a.nr, r_lo + a.split_len);
-    const int ntiles = (int)((r_hi - r_lo + TC_BN - 1) / TC_BN);
+    const int ntiles_all = (int)((r_hi - r_lo + TC_BN - 1) / TC_BN);
+    const int pblk = (int)(blockIdx.x >> 1);  // 256-row query block of this CTA (both CTAs of a pair)
+    const int ntiles = a.tile_count ? a.tile_count[pblk] : ntiles_all;
+    const int32_t* tlist = a.tile_count ? a.tile_list + (int64_t)pblk * a.tile_ld : nullptr;
     const int KB = a.kblocks;
 
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
@@ -322,7 +332,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
-                const int y_r = (int)(r_lo + (int64_t)t * TC_BN);
+                const int y_r = (int)(r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN);
                 for (int kb = 0; kb < KB; ++kb) {
 #pragma unroll
                     for (int part = 0; part < PARTS; ++part, ++g) {
@@ -425,22 +435,28 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
-            const int64_t rb = r_lo + (int64_t)t * TC_BN;
+            const int64_t rb = r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
             for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
-                const float rn_l = (jb + lane < r_hi) ? __ldg(a.rnorm + jb + lane) : INFINITY;
+                const int valid_cols = (int)imin64(32, r_hi - jb);
+                const float rn_l = lane < valid_cols ? __ldg(a.rnorm + jb + lane) : 0.0f;
+                // the accumulator holds -d2~/2 (norms folded into the GEMM); pre-filter with the
+                // chunk's largest margin: -2 acc - E_max > tmax  =>  above every threshold
+                float rmax = rn_l;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                const float vlim = -0.5f * (tmax + c_m * (qn + rmax));
                 uint32_t cm = 0;  // columns possibly below the largest threshold
 #pragma unroll
                 for (int u = 0; u < 32; ++u) {
-                    const float rn = __shfl_sync(0xffffffffu, rn_l, u);
-                    const float sq = qn + rn;
-                    v[u] = fmaf(-2.0f, v[u], sq);
-                    cm |= (uint32_t)(v[u] - c_m * sq < tmax) << u;
+                    v[u] = -2.0f * v[u];  // d2~ (exact scaling)
+                    cm |= (uint32_t)(v[u] <= -2.0f * vlim) << u;
                 }
+                if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
                 if (!valid) cm = 0;
                 if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
                 if (__reduce_max_sync(0xffffffffu, (unsigned)__popc(cm)) >= (unsigned)a.dense_min) {
@@ -498,6 +514,51 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 a.hist[q * k + t] = Hs[t * TC_BM + row] + Hs[(TC_KT + t) * TC_BM + row];
         }
         if (valid) a.amb_count[q * 2 + half] = n_amb;
+    } else if constexpr (MODE == 2) {
+        // ---------------------------------------------------- coarse tile flags (warps 2..9)
+        // Single-BF16 pass over the hi operands (norms folded: accumulator = -d2~/2, error
+        // <= a.margin (|q|^2 + |r|^2)).  A tile is flagged for the split-precision pass when
+        // some row of the 256-row block may have a column at or below its largest threshold.
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quad * 32 + lane;
+        const int64_t q = q0 + row;
+        const bool valid = q < a.nq;
+        const float qn = valid ? a.qnorm[q] : 0.0f;
+        const float tmax = valid ? a.thr_d2[q * a.k + (a.k - 1)] : -INFINITY;
+        for (int t = 0; t < ntiles; ++t) {
+            const int b = t & 1;
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
+            tc_fence_after();
+            const int tile = tlist ? tlist[t] : t;
+            const int64_t rb = r_lo + (int64_t)tile * TC_BN;
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
+            bool hit = false;
+#pragma unroll 1
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2); c += 32) {
+                float v[32];
+                tmem_ld32(taddr + c, v);
+                const int64_t jb = rb + c;
+                const int valid_cols = (int)imin64(32, r_hi - jb);
+                const float rn_l = lane < valid_cols ? __ldg(a.rnorm + jb + lane) : 0.0f;
+                float rmax = rn_l;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                const float vlim = -0.5f * (tmax + a.margin * (qn + rmax));
+                uint32_t cm = 0;
+#pragma unroll
+                for (int u = 0; u < 32; ++u) cm |= (uint32_t)(v[u] >= vlim) << u;
+                if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
+                hit |= valid && cm != 0;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (__any_sync(0xffffffffu, hit) && lane == 0) a.flags[(int64_t)pblk * a.tile_ld + tile] = 1;
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(tempty0 + 8 * b, 0));
+                else mbar_arrive(tempty0 + 8 * b);
+            }
+        }
     } else {
         // ---------------------------------------------------- epilogue (warps 2..9)
         // Warp w reads TMEM lane quadrant w % 4 (hardware restriction) and half
@@ -523,7 +584,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
-            const int64_t rb = r_lo + (int64_t)t * TC_BN;
+            const int64_t rb = r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
             for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
@@ -648,6 +709,22 @@ __global__ void colsum_kernel(const float* __restrict__ X, int64_t n, int d, dou
     }
 }
 
+// the six folded-norm columns at d_pad-6 .. d_pad-1: role 1 (A) [n1 n2 n3 1 1 1], role 2 (B)
+// [1 1 1 n1 n2 n3] with n1 + n2 + n3 = -nrm / 2 (three BF16 pieces); lanes 0..5 write
+__device__ __forceinline__ void write_norm_extras(__nv_bfloat16* rowp, int d_pad, float nrm, int role, int lane)
+{
+    if (role == 0 || lane >= 6) return;
+    const float nh = -0.5f * nrm;
+    const __nv_bfloat16 n1 = __float2bfloat16_rn(nh);
+    const float r1 = nh - __bfloat162float(n1);
+    const __nv_bfloat16 n2 = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 n3 = __float2bfloat16_rn(r1 - __bfloat162float(n2));
+    const int j = lane < 3 ? lane : lane - 3;
+    const __nv_bfloat16 piece = j == 0 ? n1 : (j == 1 ? n2 : n3);
+    const bool norm_slot = (role == 1) == (lane < 3);
+    rowp[(d_pad - 6) + lane] = norm_slot ? piece : __float2bfloat16_rn(1.0f);
+}
+
 // role 1 (query / A operand): padding columns d_pad-6 .. d_pad-1 = [n1, n2, n3, 1, 1, 1];
 // role 2 (reference / B operand): [1, 1, 1, n1, n2, n3], where n1 + n2 + n3 = -|x_c|^2 / 2 in
 // three BF16 pieces (24 significant bits).  The GEMM then accumulates
@@ -672,18 +749,8 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
-    if (role && lane < 6) {
-        const float nh = -0.5f * acc;
-        const __nv_bfloat16 n1 = __float2bfloat16_rn(nh);
-        const float r1 = nh - __bfloat162float(n1);
-        const __nv_bfloat16 n2 = __float2bfloat16_rn(r1);
-        const __nv_bfloat16 n3 = __float2bfloat16_rn(r1 - __bfloat162float(n2));
-        const __nv_bfloat16 one = __float2bfloat16_rn(1.0f);
-        const int j = lane < 3 ? lane : lane - 3;
-        const __nv_bfloat16 piece = j == 0 ? n1 : (j == 1 ? n2 : n3);
-        const bool norm_slot = (role == 1) == (lane < 3);
-        Xc[row * d_pad + (d_pad - 6) + lane] = norm_slot ? piece : one;
-    }
+    __syncwarp();
+    write_norm_extras(Xc + row * d_pad, d_pad, acc, role, lane);
 }
 
 // split-BF16 operands for the RANK mode: x_c = x - mean (fp32), hi = bf16(x_c),
@@ -693,7 +760,7 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
 __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
                                   const double* __restrict__ colsum, double inv_n,
                                   __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms,
-                                  const int32_t* __restrict__ rowmap)
+                                  const int32_t* __restrict__ rowmap, int role)
 {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -714,6 +781,8 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
+    __syncwarp();
+    write_norm_extras(o, d_pad, acc, role, lane);  // folded norms in the hi part; lo stays 0 there
 }
 
 // ----------------------------------------------------------------------------- re-rank
@@ -959,7 +1028,7 @@ umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcAr
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
-    ProfScope ps(MODE == 0 ? PROF_KNN_TC : PROF_TRUST_TC, s);
+    ProfScope ps(MODE == 0 ? PROF_KNN_TC : (MODE == 1 ? PROF_TRUST_TC : PROF_TRUST_COARSE), s);
     if constexpr (CG == 2) {
         grid.x = (grid.x + 1) & ~1u;  // whole pairs; a pair's second block may lie past n_q (masked)
         cudaLaunchConfig_t cfg{};
@@ -1081,6 +1150,36 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
 // *overflow != 0 tells the caller to fall back to the exact SIMT kernel.
 namespace {
 
+// flags [nb][nt] -> ordered list of the flagged tiles of each block (one CTA per block)
+__global__ void compact_flags_kernel(const uint8_t* __restrict__ flags, int nt, int32_t* __restrict__ list,
+                                     int32_t* __restrict__ count)
+{
+    __shared__ int base;
+    const int64_t b = blockIdx.x;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < nt; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        const bool f = t < nt && flags[b * nt + t];
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        __shared__ int wcnt[32];
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < warp; ++w) off += wcnt[w];
+        if (f) list[b * nt + off + __popc(bal & ((1u << lane) - 1u))] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += wcnt[w];
+            base += tot;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) count[b] = base;
+}
+
 __global__ void order_maps_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ pos_of)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1144,7 +1243,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     *overflow = 0;
     if (rows == 0) return UMAP_OK;
     if (k > TC_KT) { *overflow = 1; return UMAP_OK; }
-    const int d_pad = (d + TC_BK - 1) / TC_BK * TC_BK;
+    const int d_pad = (d + 6 + TC_BK - 1) / TC_BK * TC_BK;  // >= 6 padding columns for the folded norms
     const int dk = 2 * d_pad;
     Scratch colsum, xr, rn, xq, qn, amb, ambc;
     Scratch perm, pos_of, keys, qperm, qrow, selfc, thr_p, thri_p, hist_p;
@@ -1183,14 +1282,14 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)n, s));
     split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n,
                                                           xr.as<__nv_bfloat16>(), rn.as<float>(),
-                                                          ordered ? perm.as<int32_t>() : nullptr);
+                                                          ordered ? perm.as<int32_t>() : nullptr, 2);
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
     split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(ordered ? X : X + row_begin * (int64_t)d, rows, d,
                                                              d_pad, colsum.as<double>(), 1.0 / (double)n,
                                                              xq.as<__nv_bfloat16>(), qn.as<float>(),
-                                                             ordered ? qrow.as<int32_t>() : nullptr);
+                                                             ordered ? qrow.as<int32_t>() : nullptr, 1);
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
@@ -1212,8 +1311,10 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     // times 1.1 (C2: 2.94e-4)
     {
         const double u = std::ldexp(1.0, -24);
+        // + the folded norms (BF16-piece representation u S / 2; the adds of the last hi MMA and
+        //   the 8 lo-stage MMAs after them onto partial sums up to S: 144 products)
         const double c = 3.0 * std::ldexp(1.0, -16) * 0.5 + 3.0 * d_pad * 2.0 * u * 0.5 +
-                         ((d + 31) / 32 + 5) * u + (d + 1.0) * u * 2.0 + 2.0 * u;
+                         ((d + 31) / 32 + 5) * u + (d + 1.0) * u * 2.0 + 2.0 * u + 0.5 * u + 144.0 * 2.0 * u;
         a.margin = (float)(1.1 * c);
     }
     a.thr_d2 = thr_use; a.k = k;
@@ -1223,6 +1324,45 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     a.dense_min = TC_DENSE_MIN;
     if (const char* dm = getenv("UMAP_TC_DENSE_MIN")) a.dense_min = atoi(dm);  // tuning knob
     a.amb_count = ambc.as<int>();
+    // coarse pass (ordered runs): single-BF16 GEMM over the hi operands flags the
+    // reference tiles where some row of a 256-row block may reach its largest threshold; the
+    // split-precision pass then visits only those tiles (the others are certainly above every
+    // threshold of every row of the block and add nothing to any count)
+    Scratch flags, tl, tcnt;
+    const int64_t nqb = (qblocks + 1) / 2, ntl = (n + TC_BN - 1) / TC_BN;
+    if (ordered && !getenv("UMAP_TC_NO_COARSE")) {
+        UMAP_TRY(flags.alloc((size_t)nqb * ntl, s));
+        UMAP_CUDA_TRY(cudaMemsetAsync(flags.p, 0, (size_t)nqb * ntl, s));
+        UMAP_TRY(tl.alloc(sizeof(int32_t) * (size_t)nqb * ntl, s));
+        UMAP_TRY(tcnt.alloc(sizeof(int32_t) * (size_t)nqb, s));
+        TcArgs ac = a;
+        ac.kblocks = d_pad / TC_BK;   // hi part only
+        ac.flags = flags.as<uint8_t>();
+        ac.tile_ld = (int)ntl;
+        {
+            // single BF16 product with folded norms: representation (2 * 2^-8 + 2^-16) S / 2,
+            // accumulation of d_pad products onto partial sums up to S, R2's own error, norms
+            const double u = std::ldexp(1.0, -24);
+            const double c = (2.0 * std::ldexp(1.0, -8) + std::ldexp(1.0, -16)) * 0.5 + d_pad * 2.0 * u +
+                             (d + 1.0) * u * 2.0 + ((d + 31) / 32 + 5) * u + 3.0 * u;
+            ac.margin = (float)(1.1 * c);
+        }
+        UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
+        compact_flags_kernel<<<(unsigned)nqb, 256, 0, s>>>(flags.as<uint8_t>(), (int)ntl, tl.as<int32_t>(),
+                                                          tcnt.as<int32_t>());
+        UMAP_LAUNCH_CHECK("compact_flags_kernel");
+        a.tile_list = tl.as<int32_t>();
+        a.tile_count = tcnt.as<int32_t>();
+        a.tile_ld = (int)ntl;
+        if (getenv("UMAP_TC_COARSE_DEBUG")) {
+            std::vector<int32_t> cn((size_t)nqb);
+            cudaMemcpyAsync(cn.data(), tcnt.p, sizeof(int32_t) * nqb, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            double m = 0;
+            for (int32_t x : cn) m += x;
+            fprintf(stderr, "[coarse] %.1f of %lld tiles kept per block\n", m / nqb, (long long)ntl);
+        }
+    }
     UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
         ProfScope ps(PROF_RANK_FIX, s);
