@@ -118,9 +118,10 @@ def peaks():
 
 
 # library profile slot -> kernel name in the ncu summaries (profiles/ncu_*.json)
-NCU_NAME = {"knn_tc_kernel (kNN candidates)": "knn_tc_kernel<32, 4, 0>",
-            "knn_tc_kernel (trust ranks)": "knn_tc_kernel<32, 4, 1>",
-            "sgd_persistent_kernel": "sgd_persistent_kernel", "rank_fix_kernel": "rank_fix_kernel",
+NCU_NAME = {"knn_tc_kernel (kNN candidates)": "knn_tc_kernel<32, 6, 0",
+            "knn_tc_kernel (trust ranks)": "knn_tc_kernel<32, 6, 1",
+            "knn_tc_kernel (trust coarse)": "knn_tc_kernel<32, 6, 2",
+            "sgd_persistent_kernel": "sgd_persistent_kernel", "rank_fix_kernel": "rank_fix",
             "rerank_kernel": "rerank_kernel", "thresholds_warp_kernel": "thresholds_warp_kernel",
             "grid_knn_kernel": "grid_knn_kernel", "smooth_knn_kernel": "smooth_knn_kernel"}
 
@@ -150,19 +151,23 @@ def cfg_of(name):
     return c
 
 
-def kernel_work(slot, c, st, n_amb):
-    """Algorithmic work of one step of a kernel (DESIGN.md 7): (bound, amount, unit)."""
+def kernel_work(slot, c, st, n_amb, fine_frac=1.0):
+    """Algorithmic work of one step of a kernel (DESIGN.md 8): (bound, amount, unit)."""
     n, d, k, N, m, dim = c["n"], c["d"], c["k"], c["n_epochs"], 5, 2
+    if slot == "knn_tc_kernel (trust ranks)":             # the contraction over the tiles it visits
+        return "tensor", 2.0 * n * n * d * fine_frac, "flop"
     if slot.startswith("knn_tc_kernel"):
         return "tensor", 2.0 * n * n * d, "flop"          # the n x n x d distance contraction, unpadded
     if slot == "sgd_persistent_kernel":                    # SURVEY 8(d) byte model
         return "hbm", 8.0 * st["nnz"] * (N - 1) + 4.0 * dim * (m + 1) * st["positives"] + 8.0 * dim * n * (N - 1), "B"
+    # row gathers: mostly served by L2 (Morton / candidate locality), so the HBM fraction is
+    # reported separately and may exceed 1 (see `frac_of_hbm`)
     if slot == "rank_fix_kernel":
-        return "hbm", 4.0 * d * n_amb, "B"                 # one fp32 reference row per re-checked pair
+        return "gather", 4.0 * d * n_amb, "B"              # one fp32 reference row per re-checked pair
     if slot == "rerank_kernel":
-        return "hbm", 4.0 * d * n * max(32, 2 * k), "B"   # k' candidate rows per query
+        return "gather", 4.0 * d * n * max(32, 2 * k), "B"  # k' candidate rows per query
     if slot == "thresholds_warp_kernel":
-        return "hbm", 4.0 * d * n * 15, "B"                # one row per embedding neighbour
+        return "gather", 4.0 * d * n * 15, "B"             # one row per embedding neighbour
     if slot == "smooth_knn_kernel":
         return "hbm", 16.0 * n * k, "B"                    # dist + idx in, w + col out
     return None, None, None
@@ -308,6 +313,7 @@ def run_ours(args):
     clocks.mark_end()
     launches = U.kernel_launch_count() - launches0
     n_amb = U.trust_ambiguous_count()
+    fine_frac = U.trust_fine_fraction()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     ms = sum(ms_steps) / len(ms_steps)
     if world > 1:
@@ -366,21 +372,26 @@ def run_ours(args):
     kernels = {}
     for name, (tot, cnt) in prof.items():
         per = tot / args.steps
-        bound, work, unit = kernel_work(name, c, st, n_amb)
+        bound, work, unit = kernel_work(name, c, st, n_amb, fine_frac)
         rec = {"ms_per_step": per, "launches_per_step": cnt / args.steps, "share_of_step": per / ms}
         if bound == "tensor":
-            peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-            rec.update(bound="tensor", achieved=work / (per / 1e3) / 1e12, peak=peak, unit="TFLOP/s")
+            # burst peak: the measured sustained figure (4 s of back-to-back 8192^3 cuBLAS) sits below
+            # what these 5-12 ms kernels reach inside a 44 ms step at ~1950 MHz
+            rec.update(bound="tensor", achieved=work / (per / 1e3) / 1e12, peak=pk.get("bf16_tflops"),
+                       unit="TFLOP/s")
+            rec["frac"] = rec["achieved"] / rec["peak"]
         elif bound == "hbm":
             rec.update(bound="hbm", achieved=work / (per / 1e3) / 1e9, peak=pk["hbm_gbs"], unit="GB/s")
-        if bound:
             rec["frac"] = rec["achieved"] / rec["peak"]
+        elif bound == "gather":
+            rec.update(bound="gather (L2-served)", achieved=work / (per / 1e3) / 1e9, unit="GB/s",
+                       frac_of_hbm=work / (per / 1e3) / 1e9 / pk["hbm_gbs"])
         kernels[name] = rec
     dom = max(kernels, key=lambda kk: kernels[kk]["ms_per_step"]) if kernels else None
     roof = None
     if dom:
         r = kernels[dom]
-        bound, work, unit = kernel_work(dom, c, st, n_amb)
+        bound, work, unit = kernel_work(dom, c, st, n_amb, fine_frac)
         traffic, tsrc = profile_traffic(dom)
         launches_dom = max(1.0, r["launches_per_step"])
         roof = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"), "peak": r.get("peak"),
@@ -388,7 +399,7 @@ def run_ours(args):
                 "traffic": traffic,
                 "traffic_source": tsrc, "algorithmic_per_launch": (work / launches_dom) if work else None,
                 "algorithmic_unit": unit, "duration_ms_per_launch": r["ms_per_step"] / launches_dom,
-                "peak_source": pk_kind + (" bf16 sustained (kernel timed inside a long step)"
+                "peak_source": pk_kind + (" bf16 burst (the sustained figure is below what these kernels reach)"
                                           if r.get("bound") == "tensor" else " HBM copy bandwidth")}
     sgd_bytes = 8.0 * st["nnz"] * (N - 1) + 4 * 2 * 6 * positives + 8 * 2 * n * (N - 1)
     line = {
@@ -407,6 +418,7 @@ def run_ours(args):
         "sgd_edge_updates_per_s": positives / sgd_s if sgd_s > 0 else None,
         "sgd_hbm_model_frac": (sgd_bytes / sgd_s / 1e9) / pk["hbm_gbs"] if sgd_s > 0 else None,
         "positives": positives, "nnz": st["nnz"], "trustworthiness": T, "trust_ambiguous_pairs": n_amb,
+        "trust_fine_tile_fraction": fine_frac,
         "roofline": roof,
         "kernels": kernels,
         "gpu_launches": int(launches),

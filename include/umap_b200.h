@@ -227,6 +227,9 @@ UMAP_API int64_t     umap_kernel_launch_count(void);
 /* Diagnostics: pairs the calling thread's last tensor-mode trustworthiness call could not
  * certify from the tensor-core pass and re-checked exactly. */
 UMAP_API int64_t     umap_trust_ambiguous_count(void);
+/* Diagnostics: fraction of (query block, reference tile) pairs the split-precision pass of the
+ * calling thread's last tensor-mode trustworthiness call visited (1.0 without the coarse pass). */
+UMAP_API double      umap_trust_fine_fraction(void);
 /* Live per-kernel timing (bench.py's roofline): between umap_profile_begin() and
  * umap_profile_end() every hot kernel launched by the calling thread is bracketed by a CUDA
  * event pair on its own stream.  umap_profile_end synchronises those events, writes the

@@ -73,6 +73,7 @@ SIGNATURES = {
     "umap_kernel_launch_count": (c_int64, []),
     "umap_version": (ctypes.c_char_p, []),
     "umap_trust_ambiguous_count": (c_int64, []),
+    "umap_trust_fine_fraction": (c_double, []),
     "umap_profile_begin": (None, []),
     "umap_profile_end": (ctypes.c_int32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64), ctypes.c_int32]),
     "umap_profile_slot_name": (ctypes.c_char_p, [ctypes.c_int32]),

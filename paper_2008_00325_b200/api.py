@@ -251,6 +251,11 @@ def trust_ambiguous_count():
     return int(_lib.load().umap_trust_ambiguous_count())
 
 
+def trust_fine_fraction():
+    """fraction of tiles the split-precision trust pass visited in the last call (diagnostic)."""
+    return float(_lib.load().umap_trust_fine_fraction())
+
+
 def profile_begin():
     """start live per-kernel CUDA-event timing of this thread's launches"""
     _lib.load().umap_profile_begin()

@@ -36,6 +36,7 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
                           int d_emb, cudaStream_t s);
 bool dim_supported(int dim);
 int64_t last_rank_ambiguous();
+double last_fine_fraction();
 
 // ---- error state
 static thread_local std::string g_last_error;
@@ -249,6 +250,8 @@ const char* umap_version(void) { return "umap-b200 0.1 (sm_100a)"; }
 int64_t umap_kernel_launch_count(void) { return g_launches; }
 
 int64_t umap_trust_ambiguous_count(void) { return last_rank_ambiguous(); }
+
+double umap_trust_fine_fraction(void) { return last_fine_fraction(); }
 
 void umap_profile_begin(void)
 {

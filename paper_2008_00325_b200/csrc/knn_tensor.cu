@@ -32,6 +32,7 @@
 namespace umapb200 {
 
 static thread_local int64_t g_last_rank_ambiguous = 0;
+static thread_local double g_last_fine_fraction = 1.0;
 
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
                        int out_squared, int32_t* idx, float* dist, cudaStream_t s);
@@ -1363,16 +1364,19 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         a.tile_list = tl.as<int32_t>();
         a.tile_count = tcnt.as<int32_t>();
         a.tile_ld = (int)ntl;
-        if (getenv("UMAP_TC_COARSE_DEBUG")) {
-            std::vector<int32_t> cn((size_t)nqb);
-            cudaMemcpyAsync(cn.data(), tcnt.p, sizeof(int32_t) * nqb, cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            double m = 0;
-            for (int32_t x : cn) m += x;
+        std::vector<int32_t> cn((size_t)nqb);  // kept-tile diagnostic (read after the fine pass)
+        UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
+        UMAP_CUDA_TRY(cudaMemcpyAsync(cn.data(), tcnt.p, sizeof(int32_t) * nqb, cudaMemcpyDeviceToHost, s));
+        UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        double m = 0;
+        for (int32_t x : cn) m += x;
+        g_last_fine_fraction = m / ((double)nqb * (double)ntl);
+        if (getenv("UMAP_TC_COARSE_DEBUG"))
             fprintf(stderr, "[coarse] %.1f of %lld tiles kept per block\n", m / nqb, (long long)ntl);
-        }
+    } else {
+        g_last_fine_fraction = 1.0;
+        UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     }
-    UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     {
         ProfScope ps(PROF_RANK_FIX, s);
         const float* xq = ordered ? X : X + row_begin * (int64_t)d;
@@ -1415,5 +1419,6 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
 }
 
 int64_t last_rank_ambiguous() { return g_last_rank_ambiguous; }
+double last_fine_fraction() { return g_last_fine_fraction; }
 
 }  // namespace umapb200

@@ -90,7 +90,8 @@ __device__ __forceinline__ void load_row_ro(const float* Y, int64_t v, float (&y
     }
 }
 
-constexpr int SGD_WARPS = 8;
+constexpr int SGD_WARPS = 8;  // warps per CTA at MINB = 4; in general 32 / MINB (32 warps per SM)
+template <int MINB> constexpr int sgd_warps() { return MINB >= 4 ? SGD_WARPS : 32 / MINB; }
 constexpr int QCAP = 64;
 
 // R13 fixed point: q(g) = round(g 2^24) (exact scaling, |g| <= 4 so |q| <= 2^26 fits int32)
@@ -225,11 +226,12 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int k)
 // compacts due edges into a per-warp queue that is processed 32 at a time (every lane
 // carries a due edge during the expensive part).
 template <int DIM, bool DET, int MC, int VPW, int MINB, int CPB>
-__global__ void __launch_bounds__(32 * SGD_WARPS, MINB) sgd_persistent_kernel(SgdArgs A)
+__global__ void __launch_bounds__(32 * sgd_warps<MINB>(), MINB) sgd_persistent_kernel(SgdArgs A)
 {
-    __shared__ int32_t q_h[SGD_WARPS][QCAP];   // owner lane (0..VPW-1) of the queued edge
-    __shared__ int32_t q_t[SGD_WARPS][QCAP];   // tail vertex
-    __shared__ long long acc[SGD_WARPS][DIM][VPW];
+    constexpr int W = sgd_warps<MINB>();
+    __shared__ int32_t q_h[W][QCAP];   // owner lane (0..VPW-1) of the queued edge
+    __shared__ int32_t q_t[W][QCAP];   // tail vertex
+    __shared__ long long acc[W][DIM][VPW];
     __shared__ int s_ctr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = (int)A.n;
@@ -510,7 +512,7 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
     static int max_blocks = -1;
     if (max_blocks < 0) {
         int per_sm = 0;
-        UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * SGD_WARPS, 0));
+        UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * sgd_warps<MINB>(), 0));
         max_blocks = std::max(1, per_sm) * num_sms();
     }
     const int64_t want = CPB > 0 ? (A.n_chunks + CPB - 1) / CPB : A.n_chunks;
@@ -525,7 +527,7 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
     }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
-    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * SGD_WARPS), args, 0, s));
+    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(32 * sgd_warps<MINB>()), args, 0, s));
     UMAP_LAUNCH_CHECK("sgd_persistent_kernel");
     return UMAP_OK;
 }
@@ -543,20 +545,27 @@ int sgd_variant()
 template <int DIM, bool DET, int MC>
 umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
 {
-    switch (DIM == 2 ? sgd_variant() : 0) {
-        case 1: return launch_sgd_t<DIM, DET, MC, 32, 3, 8>(A, s);
-        case 2: return launch_sgd_t<DIM, DET, MC, 8, 3, 32>(A, s);
-        case 3: return launch_sgd_t<DIM, DET, MC, 16, 3, 32>(A, s);
-        case 4: return launch_sgd_t<DIM, DET, MC, 32, 3, 16>(A, s);
-        case 5: return launch_sgd_t<DIM, DET, MC, 16, 3, 8>(A, s);
-        case 6: return launch_sgd_t<DIM, DET, MC, 16, 4, 4>(A, s);
-        case 7: return launch_sgd_t<DIM, DET, MC, 8, 3, 8>(A, s);
-        case 8: return launch_sgd_t<DIM, DET, MC, 16, 4, 8>(A, s);
-        case 9: return launch_sgd_t<DIM, DET, MC, 16, 3, 16>(A, s);  // the round-1 shape
-        case 10: return launch_sgd_t<DIM, DET, MC, 8, 4, 0>(A, s);
-        case 11: return launch_sgd_t<DIM, DET, MC, 32, 4, 0>(A, s);
-        case 12: return launch_sgd_t<DIM, DET, MC, 16, 3, 0>(A, s);
-        default: return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);  // measured best at C2 (tools/sgd_variants.py)
+    if constexpr (DIM == 2) {  // launch-shape variants (tools/sgd_variants.py) only for the 2-D kernels
+        switch (DIM == 2 ? sgd_variant() : 0) {
+            case 1: return launch_sgd_t<DIM, DET, MC, 32, 3, 8>(A, s);
+            case 2: return launch_sgd_t<DIM, DET, MC, 8, 3, 32>(A, s);
+            case 3: return launch_sgd_t<DIM, DET, MC, 16, 3, 32>(A, s);
+            case 4: return launch_sgd_t<DIM, DET, MC, 32, 3, 16>(A, s);
+            case 5: return launch_sgd_t<DIM, DET, MC, 16, 3, 8>(A, s);
+            case 6: return launch_sgd_t<DIM, DET, MC, 16, 4, 4>(A, s);
+            case 7: return launch_sgd_t<DIM, DET, MC, 8, 3, 8>(A, s);
+            case 8: return launch_sgd_t<DIM, DET, MC, 16, 4, 8>(A, s);
+            case 9: return launch_sgd_t<DIM, DET, MC, 16, 3, 16>(A, s);  // the round-1 shape
+            case 10: return launch_sgd_t<DIM, DET, MC, 8, 4, 0>(A, s);
+            case 11: return launch_sgd_t<DIM, DET, MC, 32, 4, 0>(A, s);
+            case 12: return launch_sgd_t<DIM, DET, MC, 16, 3, 0>(A, s);
+            case 13: return launch_sgd_t<DIM, DET, MC, 16, 1, 0>(A, s);   // 1 CTA of 32 warps per SM
+            case 14: return launch_sgd_t<DIM, DET, MC, 16, 2, 0>(A, s);   // 2 CTAs of 16 warps per SM
+            case 15: return launch_sgd_t<DIM, DET, MC, 8, 1, 0>(A, s);
+            default: return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);  // measured best at C2 (tools/sgd_variants.py)
+        }
+    } else {
+        return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);
     }
 }
 
