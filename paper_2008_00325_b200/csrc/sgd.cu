@@ -559,10 +559,11 @@ umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
             case 10: return launch_sgd_t<DIM, DET, MC, 8, 4, 0>(A, s);
             case 11: return launch_sgd_t<DIM, DET, MC, 32, 4, 0>(A, s);
             case 12: return launch_sgd_t<DIM, DET, MC, 16, 3, 0>(A, s);
-            case 13: return launch_sgd_t<DIM, DET, MC, 16, 1, 0>(A, s);   // 1 CTA of 32 warps per SM
-            case 14: return launch_sgd_t<DIM, DET, MC, 16, 2, 0>(A, s);   // 2 CTAs of 16 warps per SM
+                case 14: return launch_sgd_t<DIM, DET, MC, 16, 2, 0>(A, s);   // 2 CTAs of 16 warps per SM
             case 15: return launch_sgd_t<DIM, DET, MC, 8, 1, 0>(A, s);
-            default: return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);  // measured best at C2 (tools/sgd_variants.py)
+            case 16: return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);  // 4 CTAs of 8 warps per SM
+            default: return launch_sgd_t<DIM, DET, MC, 16, 1, 0>(A, s);  // 1 CTA of 32 warps per SM: measured
+                                                                         // best at C2 (tools/sgd_variants.py)
         }
     } else {
         return launch_sgd_t<DIM, DET, MC, 16, 4, 0>(A, s);
