@@ -436,3 +436,47 @@ def test_c2_full_size_trust_tensor_equals_exact(O):
         S_r, pen_r = U.trust_penalty(Xg, emb_idx[r:r + 1].contiguous(), 15, r, r + 1, knn_mode="tensor", Y=Y)
         S_o, _ = O.trust_penalty(X, Yh, 15, r, r + 1)
         assert S_r == S_o, r
+
+
+@pytest.mark.slow
+def test_c3_full_size_trust_and_knn(O):
+    """C3 (60,000 x 3,072, d beyond the K-tile ring, trust k = 5) at full size: tensor-mode
+    trust S equals the exact-mode S; sampled kNN rows bit-exact against the oracle."""
+    X = synth.make("C3")
+    Xg = cu(X)
+    Y, st = U.fit(Xg, n_neighbors=15, n_epochs=200, seed=0, knn_mode="tensor", trust_k=5)
+    T_exact, S_exact = U.trustworthiness(Xg, Y, 5, knn_mode="exact")
+    assert st["trust_penalty"] == S_exact
+    gi, gd = U.knn(Xg, Xg, 15, exclude_self=True, mode="tensor")
+    gi, gd = np_(gi), np_(gd)
+    for r in np.random.default_rng(2).choice(60000, 4, replace=False):
+        ri, rd = O.knn(X[r:r + 1], X, 15, self_offset=int(r))
+        assert np.array_equal(gi[r], ri[0]) and np.array_equal(gd[r], rd[0])
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled_knn(O):
+    """C4 (1,000,000 x 50, d % 4 != 0: the per-lane re-rank path) at full size, the kNN the
+    sharded mode distributes: sampled rows bit-exact against the oracle."""
+    X = synth.make("C4")
+    gi, gd = U.knn(cu(X), cu(X), 15, exclude_self=True, mode="tensor")
+    gi, gd = np_(gi), np_(gd)
+    for r in np.concatenate([[0, 999999], np.random.default_rng(3).choice(1000000, 4, replace=False)]):
+        ri, rd = O.knn(X[r:r + 1], X, 15, self_offset=int(r))
+        assert np.array_equal(gi[r], ri[0]) and np.array_equal(gd[r], rd[0])
+
+
+@pytest.mark.slow
+def test_c5_transform_chunk_sampled_rows(O):
+    """C5: fit on the 100,000 training rows, transform one 1,000,000-row chunk of the
+    8,000,000-row set on the device (global query ids), sampled rows against the oracle."""
+    model = synth.lowrank_model(784, 10, 4)
+    Xtr = synth.lowrank_sample(model, 100000, 40)
+    Xg = cu(Xtr)
+    Ytr, _ = U.fit(Xg, n_neighbors=15, n_epochs=200, knn_mode="tensor", a=A_, b=B_)
+    Xq = synth.lowrank_sample_device(model, 1000000, 44)
+    Yq = U.transform(Xg, Ytr, Xq, q_offset=3000000, n_neighbors=15, n_epochs=200, knn_mode="tensor", a=A_, b=B_)
+    Ytr_h = np_(Ytr)
+    for r in (0, 123457, 999999):
+        yo = O.transform(Xtr, Ytr_h, np_(Xq[r:r + 1]), k=15, n_epochs=200, a=A_, b=B_, seed=0, q_offset=3000000 + r)
+        assert np.abs(np_(Yq[r]) - yo[0]).max() < 1e-3
