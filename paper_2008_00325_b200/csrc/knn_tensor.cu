@@ -45,6 +45,11 @@ constexpr int TC_BK = 64;         // K slab = 64 bf16 = 128 B (one SWIZZLE_128B 
 constexpr int TC_KCMAX = 64;      // max candidates per query row (k')
 constexpr int TC_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, each half of the columns
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;   // producer + MMA + epilogue warps
+// epilogue warps per MODE: the trust fine pass (MODE 1) is latency-bound in its bucketing,
+// so it runs four warps per TMEM lane quadrant (a quarter of the columns each)
+template <int MODE> constexpr int tc_epi_warps() { return MODE == 1 ? 16 : TC_EPI_WARPS; }
+template <int MODE> constexpr int tc_threads() { return 64 + 32 * tc_epi_warps<MODE>(); }
+template <int MODE> constexpr int tc_amb_lists() { return tc_epi_warps<MODE>() / 4; }  // per row
 constexpr uint32_t A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr uint32_t B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -261,7 +266,7 @@ constexpr int TC_DENSE_MIN = 16;  // a warp whose busiest lane has this many can
 // by a third; the leader (rank 0) issues the MMAs, each CTA's TMEM holds its 128 rows x
 // 256 columns, and each CTA's epilogue filters its own rows exactly as for CG = 1.
 template <int KC, int TC_STAGES, int MODE, int CG>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(tc_threads<MODE>(), 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_r, TcArgs a)
 {
     constexpr uint32_t B_ROWS = TC_BN / CG;                     // reference rows loaded by this CTA
@@ -295,7 +300,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, CG * TC_EPI_WARPS);  // the epilogue warps of every CTA of the pair
+            mbar_init(tempty0 + 8 * b, CG * tc_epi_warps<MODE>());  // the epilogue warps of every CTA of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_q) : "memory");
@@ -410,7 +415,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         // d2~ - E > thr_t.  Rows whose bucket is certain are counted in a shared histogram;
         // the rest are appended (warp-aggregated) for an exact re-check.
         const int quad = warp & 3;
-        const int half = (warp - 2) >> 2;
+        constexpr int NP = tc_amb_lists<MODE>();            // column parts (warps per lane quadrant)
+        constexpr int CP = TC_BN / NP;                      // columns per part
+        const int half = (warp - 2) >> 2;                   // this warp's part
         const int row = quad * 32 + lane;
         const int64_t q = q0 + row;
         const bool valid = q < a.nq;
@@ -425,12 +432,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
 #pragma unroll
         for (int t = 1; t < TC_KT; ++t) tmax = (t < k) ? thr[t] : tmax;
         const float c_m = a.margin;
-        // shared histogram [half][t][row] after the ring region (ring stays untouched)
+        // shared histogram [part][t][row] after the ring region (ring stays untouched)
         int32_t* Hs = reinterpret_cast<int32_t*>(stage_base + TC_STAGES * STAGE_C + 8 * (2 * TC_STAGES + 4) + 16);
 #pragma unroll
         for (int t = 0; t < TC_KT; ++t) Hs[(half * TC_KT + t) * TC_BM + row] = 0;
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
-        int32_t* amb_row = a.amb + (valid ? (q * 2 + half) * (int64_t)a.amb_cap : 0);
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * tc_epi_warps<MODE>()) : "memory");
+        int32_t* amb_row = a.amb + (valid ? (q * NP + half) * (int64_t)a.amb_cap : 0);
         int n_amb = 0;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
@@ -439,7 +446,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int64_t rb = r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
-            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
+            for (int c = half * CP; c < (half + 1) * CP && !(a.debug & 1); c += 32) {
                 float v[32];
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
@@ -509,12 +516,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 else mbar_arrive(tempty0 + 8 * b);
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * TC_EPI_WARPS) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * tc_epi_warps<MODE>()) : "memory");
         if (half == 0 && valid) {
-            for (int t = 0; t < k; ++t)
-                a.hist[q * k + t] = Hs[t * TC_BM + row] + Hs[(TC_KT + t) * TC_BM + row];
+            for (int t = 0; t < k; ++t) {
+                int sum = 0;
+#pragma unroll
+                for (int pp = 0; pp < NP; ++pp) sum += Hs[(pp * TC_KT + t) * TC_BM + row];
+                a.hist[q * k + t] = sum;
+            }
         }
-        if (valid) a.amb_count[q * 2 + half] = n_amb;
+        if (valid) a.amb_count[q * NP + half] = n_amb;
     } else if constexpr (MODE == 2) {
         // ---------------------------------------------------- coarse tile flags (warps 2..9)
         // Single-BF16 pass over the hi operands (norms folded: accumulator = -d2~/2, error
@@ -823,9 +834,10 @@ rank_fix_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr, int 
         td[t] = t < k ? thr_d2[q * k + t] : INFINITY;
         ti[t] = t < k ? thr_id[q * k + t] : INT32_MAX;
     }
-    for (int hf = 0; hf < 2; ++hf) {
-        const int cnt = min(amb_count[q * 2 + hf], cap_row);
-        const int32_t* list = amb + (q * 2 + hf) * (int64_t)cap_row;
+    constexpr int NL = tc_amb_lists<1>();
+    for (int hf = 0; hf < NL; ++hf) {
+        const int cnt = min(amb_count[q * NL + hf], cap_row);
+        const int32_t* list = amb + (q * NL + hf) * (int64_t)cap_row;
         for (int e = lane; e < cnt; e += 32) {
             const int32_t l = colmap ? colmap[list[e]] : list[e];  // colmap: column -> input row
             const float v = exact_d2(x, Xr + (int64_t)l * d, d);
@@ -864,14 +876,21 @@ rank_fix_bulk_kernel(const float* __restrict__ Xq, const float* __restrict__ Xr,
             td[t] = t < k ? thr_d2[q * k + t] : INFINITY;
             ti[t] = t < k ? thr_id[q * k + t] : INT32_MAX;
         }
-        const int c0 = min(amb_count[q * 2], cap_row), c1 = min(amb_count[q * 2 + 1], cap_row);
-        const int32_t* list0 = amb + (q * 2) * (int64_t)cap_row;
-        const int32_t* list1 = list0 + cap_row;
-        for (int base = 0; base < c0 + c1; base += 32) {
+        // the row's lists (one per column part) taken as one sequence, 32 entries at a time
+        constexpr int NL = tc_amb_lists<1>();
+        int cnt[NL], tot = 0;
+#pragma unroll
+        for (int h = 0; h < NL; ++h) { cnt[h] = min(amb_count[q * NL + h], cap_row); tot += cnt[h]; }
+        const int32_t* lists = amb + (q * NL) * (int64_t)cap_row;
+        for (int base = 0; base < tot; base += 32) {
             const int e = base + lane;
             int32_t l = -1;
-            if (e < c0 + c1) {
-                const int32_t col = e < c0 ? list0[e] : list1[e - c0];
+            if (e < tot) {
+                int h = 0, off = e;
+#pragma unroll
+                for (int hh = 0; hh < NL - 1; ++hh)
+                    if (h == hh && off >= cnt[hh]) { off -= cnt[hh]; h = hh + 1; }
+                const int32_t col = lists[(int64_t)h * cap_row + off];
                 l = colmap ? colmap[col] : col;
             }
             const float v = exact_d2_bulk(x, Xr, l, d, ring, bar0, ph, lane);
@@ -1005,7 +1024,7 @@ template <int KC, int ST, int MODE, int CG>
 size_t knn_tc_smem_bytes()
 {
     const size_t stage = A_BYTES + (size_t)(TC_BN / CG) * TC_BK * 2;
-    return 1024 + ST * stage + 8 * (2 * ST + 4) + 16 + (MODE == 1 ? 2 * TC_KT * TC_BM * 4 + 16 : 0);
+    return 1024 + ST * stage + 8 * (2 * ST + 4) + 16 + (MODE == 1 ? tc_amb_lists<MODE>() * TC_KT * TC_BM * 4 + 16 : 0);
 }
 
 // CTA-pair MMA (cta_group::2) unless UMAP_TC_CG=1 (A/B comparison knob)
@@ -1034,7 +1053,7 @@ umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcAr
         grid.x = (grid.x + 1) & ~1u;  // whole pairs; a pair's second block may lie past n_q (masked)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
-        cfg.blockDim = dim3(TC_THREADS);
+        cfg.blockDim = dim3(tc_threads<MODE>());
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -1046,7 +1065,7 @@ umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcAr
         cfg.numAttrs = 1;
         UMAP_CUDA_TRY(cudaLaunchKernelEx(&cfg, knn_tc_kernel<KC, ST, MODE, CG>, mq, mr, a));
     } else {
-        knn_tc_kernel<KC, ST, MODE, CG><<<grid, TC_THREADS, smem, s>>>(mq, mr, a);
+        knn_tc_kernel<KC, ST, MODE, CG><<<grid, tc_threads<MODE>(), smem, s>>>(mq, mr, a);
     }
     UMAP_LAUNCH_CHECK("knn_tc_kernel");
     return UMAP_OK;
@@ -1055,7 +1074,7 @@ umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcAr
 template <int KC, int MODE>
 umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
 {
-    if (tc_cg() == 2) return launch_tc_t<KC, 6, MODE, 2>(mq, mr, a, grid, s);
+    if (tc_cg() == 2) return launch_tc_t<KC, MODE == 1 ? 5 : 6, MODE, 2>(mq, mr, a, grid, s);
     return launch_tc_t<KC, 4, MODE, 1>(mq, mr, a, grid, s);
 }
 
@@ -1303,9 +1322,10 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
     UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN / tc_cg()));
     const int64_t qblocks = (rows + TC_BM - 1) / TC_BM;
-    const int cap = 2048;
-    UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * 2 * cap, s));
-    UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * 2, s));
+    constexpr int NL = tc_amb_lists<1>();  // ambiguous-pair lists per row (one per column part)
+    const int cap = 4096 / NL;
+    UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * NL * cap, s));
+    UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * NL, s));
     const float* thr_use = ordered ? thr_p.as<float>() : thr_d2;
     const int32_t* thri_use = ordered ? thri_p.as<int32_t>() : thr_id;
     int32_t* hist_use = ordered ? hist_p.as<int32_t>() : hist;
@@ -1406,8 +1426,8 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                                                                   hist);
         UMAP_LAUNCH_CHECK("unscatter_hist_kernel");
     }
-    std::vector<int> counts((size_t)rows * 2);
-    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * 2, cudaMemcpyDeviceToHost, s));
+    std::vector<int> counts((size_t)rows * NL);
+    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * NL, cudaMemcpyDeviceToHost, s));
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
     int64_t total = 0;
     for (int c : counts) {
