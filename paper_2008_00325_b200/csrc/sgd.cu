@@ -57,6 +57,11 @@ __device__ __forceinline__ bool edge_due(float r, int e)
 {
     return floorf(__fmul_rn((float)e, r)) > floorf(__fmul_rn((float)(e - 1), r));
 }
+// the same test with the epoch conversions hoisted: ef = (float)e, ef1 = (float)(e - 1)
+__device__ __forceinline__ bool edge_due_f(float r, float ef, float ef1)
+{
+    return floorf(__fmul_rn(ef, r)) > floorf(__fmul_rn(ef1, r));
+}
 
 // positions are read through L2 only (ld.global.cg): they change between epochs of the
 // persistent kernel and L1 is not coherent
@@ -242,6 +247,7 @@ __global__ void __launch_bounds__(32 * sgd_warps<MINB>(), MINB) sgd_persistent_k
         const float* Yr = (DET && par) ? A.Y1 : A.Y0;
         float* Yw = DET ? (par ? A.Y0 : A.Y1) : A.Y0;
         const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
+        const float ef = (float)epoch, ef1 = (float)(epoch - 1);
         // a CTA owns CPB consecutive chunks (VPW * CPB vertices); its warps take chunks from
         // the CTA's range through a shared-memory counter (dynamic balance inside the CTA,
         // no global work counter: thousands of grabs per epoch would serialise at L2)
@@ -306,7 +312,7 @@ __global__ void __launch_bounds__(32 * sgd_warps<MINB>(), MINB) sgd_persistent_k
                 const int64_t e = base + lane;
                 const int2 rec = nrec;  // records are prefetched one 32-edge step ahead
                 if (base + 32 + lane < e_hi) nrec = __ldg(A.edges + base + 32 + lane);
-                const bool due = e < e_hi && edge_due(__int_as_float(rec.y), epoch);
+                const bool due = e < e_hi && edge_due_f(__int_as_float(rec.y), ef, ef1);
                 // owner lane of the edge's head vertex within the chunk (precomputed)
                 const int lo = due ? (int)(__ldg(A.owner + e) & (VPW - 1)) : 0;
                 const unsigned ballot = __ballot_sync(0xffffffffu, due);
