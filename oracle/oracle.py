@@ -247,9 +247,30 @@ def fuzzy_graph(X, k):
     return idx, dist, rho, sigma, w, fuzzy_union(idx, w)
 
 
+def supervised_adjust(indptr, col, w, labels, far_dist=5.0, unknown_dist=1.0):
+    """Label adjustment of the fuzzy union ("adjusts the membership strengths of the
+    fuzzy sets based on their labels"; rule of SPEC S:308-316, reading R17): entry (i, j) is
+    multiplied by 1 if labels[i] == labels[j] (both known), by exp(-far_dist) if both are
+    known and differ, by exp(-unknown_dist) if either is -1; entries below 1e-8 are dropped.
+    The factors are rounded to fp32 once, the products are fp32."""
+    indptr, col, w = np.asarray(indptr, np.int64), np.asarray(col, np.int32), np.asarray(w, np.float32)
+    labels = np.asarray(labels, np.int64)
+    f_far, f_unk = np.float32(math.exp(-far_dist)), np.float32(math.exp(-unknown_dist))
+    n = indptr.shape[0] - 1
+    rows = np.repeat(np.arange(n), np.diff(indptr))
+    li, lj = labels[rows], labels[col]
+    factor = np.where((li < 0) | (lj < 0), f_unk, np.where(li == lj, np.float32(1.0), f_far)).astype(np.float32)
+    w2 = (w * factor).astype(np.float32)
+    keep = w2 >= np.float32(1e-8)
+    new_indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=new_indptr[1:])
+    return new_indptr, col[keep].copy(), w2[keep].copy()
+
+
 def fit(X, k=15, n_components=2, n_epochs=None, a=None, b=None, min_dist=0.1, spread=1.0, m=5, seed=0,
-        mode="deterministic"):
-    """Whole fit: kNN -> rho/sigma -> membership -> union -> init -> SGD."""
+        mode="deterministic", labels=None, far_dist=5.0, unknown_dist=1.0):
+    """Whole fit: kNN -> rho/sigma -> membership -> union -> (labels: supervised adjustment)
+    -> init -> SGD (P:47-61, P:77, P:97-140)."""
     X = _f32(X)
     n = X.shape[0]
     if n_epochs is None:
@@ -257,6 +278,8 @@ def fit(X, k=15, n_components=2, n_epochs=None, a=None, b=None, min_dist=0.1, sp
     if a is None or b is None:
         a, b = fit_ab(min_dist, spread)
     _, _, _, _, _, (indptr, col, w) = fuzzy_graph(X, k)
+    if labels is not None:
+        indptr, col, w = supervised_adjust(indptr, col, w, labels, far_dist, unknown_dist)
     Y0 = random_init(n, n_components, seed)
     return optimize(indptr, col, w, Y0, np.float32(a), np.float32(b), n_epochs, m=m, seed=seed, mode=mode)
 

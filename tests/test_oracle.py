@@ -391,3 +391,36 @@ def test_oracle_fit_digits_shape_quality(O):
     Y = O.fit(X, k=15, n_epochs=100, a=A_, b=B_, seed=1, mode="deterministic")
     assert np.all(np.isfinite(Y))
     assert O.trustworthiness(X, Y, 15) > 0.95
+
+
+# ------------------------------------------------------------------- supervised adjustment (f4)
+def test_supervised_adjust_spec_examples():
+    """S:313-316: same labels unchanged; 0 vs 1 with far_dist = 5 -> x e^-5 (0.006738);
+    a -1 label with unknown_dist = 1 -> x e^-1."""
+    from oracle import oracle as O
+    indptr = np.array([0, 2, 4, 6], np.int64)
+    col = np.array([1, 2, 0, 2, 0, 1], np.int32)
+    w = np.array([0.5, 0.8, 0.5, 0.25, 0.8, 0.25], np.float32)
+    p, c, v = O.supervised_adjust(indptr, col, w, [0, 0, 1], far_dist=5.0, unknown_dist=1.0)
+    assert np.array_equal(p, indptr) and np.array_equal(c, col)
+    assert v[0] == w[0] and v[2] == w[2]                       # (0,1), (1,0): same label
+    assert abs(v[1] / w[1] - 0.006737947) < 1e-6               # (0,2): 0 vs 1
+    p, c, v = O.supervised_adjust(indptr, col, w, [0, -1, 0], far_dist=5.0, unknown_dist=1.0)
+    assert abs(v[0] / w[0] - math.exp(-1)) < 1e-6 and v[1] == w[1]
+
+
+def test_supervised_adjust_properties():
+    """Symmetry preserved (the rule is symmetric in (i, j)); all-equal labels are the identity;
+    tiny products are dropped below 1e-8."""
+    from oracle import oracle as O
+    X = synth.lowrank(300, 8, blobs=3, seed=5)
+    _, _, _, _, _, (indptr, col, w) = O.fuzzy_graph(X, 10)
+    p, c, v = O.supervised_adjust(indptr, col, w, np.zeros(300, np.int64))
+    assert np.array_equal(p, indptr) and np.array_equal(c, col) and np.array_equal(v, w)
+    lab = np.random.default_rng(0).integers(-1, 3, 300)
+    p, c, v = O.supervised_adjust(indptr, col, w, lab, far_dist=5.0)
+    import scipy.sparse as sp
+    B = sp.csr_matrix((v, c, p), shape=(300, 300))
+    assert abs(B - B.T).max() == 0
+    p, c, v = O.supervised_adjust(indptr, col, w, np.arange(300), far_dist=40.0)
+    assert v.size < w.size and (v >= 1e-8).all()
