@@ -86,6 +86,9 @@ typedef struct {
     int32_t  transform_epochs;     /* 0 -> ceil(n_epochs / 3) (R15)                          */
     int32_t  trust_k;              /* umap_fit only: > 0 -> also score the embedding with    */
                                    /* T(trust_k) (a10, knn_mode) into umap_fit_stats; 0 skip */
+    float    far_dist;             /* supervised (umap_fit_supervised): different labels ->  */
+                                   /* weight x exp(-far_dist), default 5.0 (R17)             */
+    float    unknown_dist;         /* a label -1 on either end -> x exp(-unknown_dist), 1.0  */
 } umap_params;
 
 /* Per-stage device times (ms, CUDA events on `stream`) and graph statistics. */
@@ -209,6 +212,21 @@ UMAP_API umap_status umap_transform_optimize(const int32_t* idx, const float* w,
                                     const float* Y_train, int64_t n_train, float* Y_q,
                                     const umap_params* p, int32_t n_epochs_t, int32_t e_begin,
                                     int32_t e_end, int64_t q_offset, int32_t init, void* stream);
+
+/* Supervised fit (R17): as umap_fit with training labels (n int32, -1 = unknown; host
+ * or device) -- between the fuzzy union (a5) and the SGD (a6-a8) every entry (i, j) of B is
+ * multiplied by 1 (same label), exp(-p->far_dist) (different known labels) or
+ * exp(-p->unknown_dist) (either unknown), entries below 1e-8 dropped. */
+UMAP_API umap_status umap_fit_supervised(const float* X, int64_t n, int32_t d, const int32_t* labels,
+                                         const umap_params* p, float* Y, umap_fit_stats* stats, void* stream);
+
+/* The label adjustment alone on a device CSR (indptr n+1 int64, col int32, val fp32): writes
+ * the adjusted CSR (out_indptr n+1, out_col / out_val with room for `capacity` entries) and
+ * *nnz (host).  UMAP_ERR_INVALID_ARGUMENT if capacity is too small. */
+UMAP_API umap_status umap_supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                                            const int32_t* labels, float far_dist, float unknown_dist,
+                                            int64_t* out_indptr, int32_t* out_col, float* out_val,
+                                            int64_t capacity, int64_t* nnz, void* stream);
 
 /* a10 input-space rank penalties for rows [row_begin, row_end) (R16): emb_idx is the
  * embedding kNN of those rows (n_rows x k, global ids).  knn_mode as in

@@ -7,8 +7,10 @@ over torch.distributed (dist.py).  There is no CPU fallback.
 from .api import (fit, fit_ab, fit_knn, fuzzy_union, kernel_launch_count, knn, optimize, params, random_init, smooth_knn,
                   topk_merge, transform, transform_optimize, trust_from_penalty, trust_penalty, trustworthiness,
                   version, default_transform_epochs, trust_ambiguous_count,
-                  profile_begin, profile_end, trust_fine_fraction)
+                  profile_begin, profile_end, trust_fine_fraction,
+                  supervised_adjust)
 
 __all__ = ["fit", "fit_ab", "fit_knn", "fuzzy_union", "kernel_launch_count", "knn", "optimize", "params", "random_init",
            "smooth_knn", "topk_merge", "transform", "transform_optimize", "trust_from_penalty", "trust_penalty",
-           "trustworthiness", "version", "default_transform_epochs", "trust_ambiguous_count", "profile_begin", "profile_end", "trust_fine_fraction"]
+           "trustworthiness", "version", "default_transform_epochs", "trust_ambiguous_count", "profile_begin", "profile_end", "trust_fine_fraction",
+           "supervised_adjust"]

@@ -43,7 +43,8 @@ def _any(t, dtype, name):
 
 def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0, negative_sample_rate=5,
            learning_rate=1.0, repulsion_strength=1.0, a=0.0, b=0.0, seed=0, sgd_mode="deterministic",
-           knn_mode="exact", knn_candidates=32, transform_epochs=0, trust_k=0) -> UmapParams:
+           knn_mode="exact", knn_candidates=32, transform_epochs=0, trust_k=0, far_dist=5.0,
+           unknown_dist=1.0) -> UmapParams:
     p = UmapParams()
     _lib.load().umap_params_default(ctypes.byref(p))
     p.n_neighbors, p.n_components, p.n_epochs = n_neighbors, n_components, n_epochs
@@ -53,6 +54,7 @@ def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0,
     p.sgd_mode = SGD_MODES[sgd_mode] if isinstance(sgd_mode, str) else sgd_mode
     p.knn_mode = KNN_MODES[knn_mode] if isinstance(knn_mode, str) else knn_mode
     p.knn_candidates, p.transform_epochs, p.trust_k = knn_candidates, transform_epochs, trust_k
+    p.far_dist, p.unknown_dist = far_dist, unknown_dist
     return p
 
 
@@ -62,10 +64,13 @@ def fit_ab(min_dist=0.1, spread=1.0):
     return a.value, b.value
 
 
-def fit(X, out=None, **kw):
+def fit(X, out=None, labels=None, **kw):
     """umap_fit: X (n x d fp32, CUDA or CPU tensor) -> (Y, stats dict). Y lives where X lives
-    unless `out` is given.  trust_k > 0 also scores Y (stats["trustworthiness"])."""
+    unless `out` is given.  trust_k > 0 also scores Y (stats["trustworthiness"]).  labels (n
+    int32, -1 = unknown): the supervised fit umap_fit_supervised (far_dist, unknown_dist)."""
     X = _any(X, torch.float32, "X")
+    if labels is not None:
+        labels = _any(labels, torch.int32, "labels")
     p = params(**kw)
     n, d = X.shape
     if out is None:
@@ -73,9 +78,31 @@ def fit(X, out=None, **kw):
                           pin_memory=(not X.is_cuda and X.is_pinned()))
     st = UmapFitStats()
     dev = X.device if X.is_cuda else out.device if out.is_cuda else None
-    check(_lib.load().umap_fit(_ptr(X), n, d, ctypes.byref(p), _ptr(out), ctypes.byref(st), _stream(dev)),
-          "umap_fit")
+    if labels is None:
+        check(_lib.load().umap_fit(_ptr(X), n, d, ctypes.byref(p), _ptr(out), ctypes.byref(st), _stream(dev)),
+              "umap_fit")
+    else:
+        check(_lib.load().umap_fit_supervised(_ptr(X), n, d, _ptr(labels), ctypes.byref(p), _ptr(out),
+                                              ctypes.byref(st), _stream(dev)), "umap_fit_supervised")
     return out, st.as_dict()
+
+
+def supervised_adjust(indptr, col, val, labels, far_dist=5.0, unknown_dist=1.0):
+    """umap_supervised_adjust on a device CSR -> (indptr, col, val) of the label-adjusted graph."""
+    indptr = _dev(indptr, torch.int64, "indptr")
+    col = _dev(col, torch.int32, "col")
+    val = _dev(val, torch.float32, "val")
+    labels = _dev(labels, torch.int32, "labels")
+    n = indptr.shape[0] - 1
+    cap = col.shape[0]
+    oi = torch.empty_like(indptr)
+    oc = torch.empty_like(col)
+    ov = torch.empty_like(val)
+    nnz = ctypes.c_int64()
+    check(_lib.load().umap_supervised_adjust(_ptr(indptr), _ptr(col), _ptr(val), n, _ptr(labels), far_dist,
+                                             unknown_dist, _ptr(oi), _ptr(oc), _ptr(ov), cap, ctypes.byref(nnz),
+                                             _stream(indptr.device)), "umap_supervised_adjust")
+    return oi, oc[:nnz.value], ov[:nnz.value]
 
 
 def fit_knn(knn_idx, knn_dist, out=None, **kw):

@@ -35,6 +35,9 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
                           int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, const float* Y,
                           int d_emb, cudaStream_t s);
 bool dim_supported(int dim);
+umap_status supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                              const int32_t* labels, float far_dist, float unknown_dist, int64_t* out_indptr,
+                              int32_t* out_col, float* out_val, int64_t capacity, int64_t* nnz_host, cudaStream_t s);
 int64_t last_rank_ambiguous();
 double last_fine_fraction();
 
@@ -324,6 +327,9 @@ void umap_params_default(umap_params* p)
     p->knn_mode = UMAP_KNN_EXACT_FP32;
     p->knn_candidates = 32;
     p->transform_epochs = 0;
+    p->trust_k = 0;
+    p->far_dist = 5.0f;
+    p->unknown_dist = 1.0f;
 }
 
 // R8: Levenberg-Marquardt least squares of Phi(x) = 1/(1 + a x^{2b}) against the
@@ -552,7 +558,7 @@ namespace {
 
 // a3..a8 from a kNN graph already on the device (idx int32, dist fp32, n x k, rows sorted).
 umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const umap_params& p, float* Yd,
-                         umap_fit_stats& st, Timer& tm, cudaStream_t s)
+                         umap_fit_stats& st, Timer& tm, cudaStream_t s, const int32_t* labels = nullptr)
 {
     const int k = p.n_neighbors, dim = p.n_components;
     // a3 + a4
@@ -570,14 +576,27 @@ umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const
     int64_t nnz = 0;
     UMAP_TRY(fuzzy_union(acol.as<int32_t>(), aw.as<float>(), n, k, indptr.as<int64_t>(), col.as<int32_t>(),
                          val.as<float>(), cap, &nnz, s));
+    Scratch sindptr, scol, sval;
+    const int64_t* g_indptr = indptr.as<int64_t>();
+    const int32_t* g_col = col.as<int32_t>();
+    const float* g_val = val.as<float>();
+    if (labels) {  // supervised: label-adjusted B (R17)
+        UMAP_TRY(sindptr.alloc(sizeof(int64_t) * (size_t)(n + 1), s));
+        UMAP_TRY(scol.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1), s));
+        UMAP_TRY(sval.alloc(sizeof(float) * (size_t)std::max<int64_t>(nnz, 1), s));
+        UMAP_TRY(supervised_adjust(g_indptr, g_col, g_val, n, labels, p.far_dist, p.unknown_dist,
+                                   sindptr.as<int64_t>(), scol.as<int32_t>(), sval.as<float>(), nnz, &nnz, s));
+        g_indptr = sindptr.as<int64_t>();
+        g_col = scol.as<int32_t>();
+        g_val = sval.as<float>();
+    }
     st.ms_union = tm.lap();
     // a7
     UMAP_TRY(random_init(n, dim, p.seed, Yd, s));
     st.ms_init = tm.lap();
     // a6 + a8
     int64_t positives = 0;
-    UMAP_TRY(optimize_layout(indptr.as<int64_t>(), col.as<int32_t>(), val.as<float>(), n, nnz, Yd, &p, 1,
-                             p.n_epochs, &positives, s));
+    UMAP_TRY(optimize_layout(g_indptr, g_col, g_val, n, nnz, Yd, &p, 1, p.n_epochs, &positives, s));
     st.ms_sgd = tm.lap();
     bool bad = false;
     UMAP_TRY(any_nonfinite(Yd, n * (int64_t)dim, &bad, s));
@@ -596,8 +615,47 @@ umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const
 
 extern "C" {
 
+static umap_status fit_impl(const float* X, int64_t n, int32_t d, const int32_t* labels, const umap_params* p_in,
+                            float* Y, umap_fit_stats* stats, void* stream);
+
 umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_params* p_in, float* Y, umap_fit_stats* stats,
                      void* stream)
+{
+    return fit_impl(X, n, d, nullptr, p_in, Y, stats, stream);
+}
+
+umap_status umap_fit_supervised(const float* X, int64_t n, int32_t d, const int32_t* labels, const umap_params* p,
+                                float* Y, umap_fit_stats* stats, void* stream)
+{
+    if (!labels) { set_last_error("labels required"); return UMAP_ERR_INVALID_ARGUMENT; }
+    return fit_impl(X, n, d, labels, p, Y, stats, stream);
+}
+
+umap_status umap_supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                                   const int32_t* labels, float far_dist, float unknown_dist, int64_t* out_indptr,
+                                   int32_t* out_col, float* out_val, int64_t capacity, int64_t* nnz, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || !indptr || !col || !val || !labels || !out_indptr || !out_col || !out_val) {
+        set_last_error("null array or n < 1");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    UMAP_TRY(require_device(indptr, "indptr"));
+    UMAP_TRY(require_device(col, "col"));
+    UMAP_TRY(require_device(val, "val"));
+    UMAP_TRY(require_device(labels, "labels"));
+    UMAP_TRY(require_device(out_indptr, "out_indptr"));
+    UMAP_TRY(require_device(out_col, "out_col"));
+    UMAP_TRY(require_device(out_val, "out_val"));
+    UMAP_TRY(supervised_adjust(indptr, col, val, n, labels, far_dist, unknown_dist, out_indptr, out_col, out_val,
+                               capacity, nnz, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
+}
+
+static umap_status fit_impl(const float* X, int64_t n, int32_t d, const int32_t* labels, const umap_params* p_in,
+                            float* Y, umap_fit_stats* stats, void* stream)
 {
     UMAP_TRY(require_cuda());
     cudaStream_t s = (cudaStream_t)stream;
@@ -626,7 +684,15 @@ umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_params* p_
     UMAP_TRY(dist.alloc(sizeof(float) * (size_t)n * k, s));
     UMAP_TRY(run_knn(&p, Xd.p, n, Xd.p, n, d, k, 0, 1, 0, 0, idx.as<int32_t>(), dist.as<float>(), s));
     st.ms_knn = tm.lap();
-    UMAP_TRY(fit_from_knn(idx.as<int32_t>(), dist.as<float>(), n, p, Yd.p, st, tm, s));
+    // labels on the device (staged if given in host memory)
+    const int32_t* lab_d = labels;
+    Scratch lab_buf;
+    if (labels && !is_device_ptr(labels)) {
+        UMAP_TRY(lab_buf.alloc(sizeof(int32_t) * (size_t)n, s));
+        UMAP_CUDA_TRY(cudaMemcpyAsync(lab_buf.p, labels, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
+        lab_d = lab_buf.as<int32_t>();
+    }
+    UMAP_TRY(fit_from_knn(idx.as<int32_t>(), dist.as<float>(), n, p, Yd.p, st, tm, s, lab_d));
     if (p.trust_k > 0) {  // a10 on the device-resident X and Y (no second staging of X)
         if (2 * (int64_t)p.trust_k >= n || p.trust_k > 64) {
             set_last_error("trust_k: 1 <= trust_k < n/2, trust_k <= 64");

@@ -9,6 +9,8 @@
 //    histogram -> scan -> scatter -> per-row sort), then a two-pointer merge of row i
 //    of A and row i of A^T applying w = (a + b) - a*b (R7), written straight into a
 //    CSR sorted by (row, col).
+#include <cmath>
+
 #include "common.cuh"
 
 namespace umapb200 {
@@ -318,6 +320,73 @@ umap_status fuzzy_union(const int32_t* acol, const float* aw, int64_t n, int k, 
     union_rows_kernel<true><<<ceil_div(n, 128), 128, 0, s>>>(acol, aw, n, k, tptr.as<int64_t>(), tsrc.as<int32_t>(),
                                                             tw.as<float>(), nullptr, indptr, col, val);
     UMAP_LAUNCH_CHECK("union_rows_kernel<fill>");
+    if (nnz_host) *nnz_host = total;
+    return UMAP_OK;
+}
+
+}  // namespace umapb200
+
+// ---------------------------------------------------------------- supervised adjustment (f4)
+// "when training labels are provided, an additional step ... adjusts the membership
+// strengths of the fuzzy sets based on their labels" (rule R17): entry (i, j)
+// times 1 (same known label), f_far = fp32(exp(-far_dist)) (different known labels) or
+// f_unk = fp32(exp(-unknown_dist)) (either label -1); products below 1e-8 are dropped.
+// Two passes over the CSR (count -> scan -> fill), thread per row; the rule is symmetric in
+// (i, j), so the result stays symmetric.
+namespace umapb200 {
+namespace {
+
+__device__ __forceinline__ float label_factor(int32_t li, int32_t lj, float f_far, float f_unk)
+{
+    return (li < 0 || lj < 0) ? f_unk : (li == lj ? 1.0f : f_far);
+}
+
+template <bool FILL>
+__global__ void supervised_rows_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ col,
+                                       const float* __restrict__ val, int64_t n, const int32_t* __restrict__ labels,
+                                       float f_far, float f_unk, int32_t* __restrict__ cnt,
+                                       const int64_t* __restrict__ out_indptr, int32_t* __restrict__ out_col,
+                                       float* __restrict__ out_val)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t li = labels[i];
+    int64_t o = FILL ? out_indptr[i] : 0;
+    int c = 0;
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+        const int32_t j = col[e];
+        const float w = __fmul_rn(val[e], label_factor(li, labels[j], f_far, f_unk));
+        if (w >= 1e-8f) {
+            if (FILL) { out_col[o] = j; out_val[o] = w; ++o; }
+            ++c;
+        }
+    }
+    if (!FILL) cnt[i] = c;
+}
+
+}  // namespace
+
+umap_status supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                              const int32_t* labels, float far_dist, float unknown_dist, int64_t* out_indptr,
+                              int32_t* out_col, float* out_val, int64_t capacity, int64_t* nnz_host, cudaStream_t s)
+{
+    const float f_far = (float)std::exp(-(double)far_dist), f_unk = (float)std::exp(-(double)unknown_dist);
+    Scratch cnt;
+    UMAP_TRY(cnt.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(n, 1), s));
+    supervised_rows_kernel<false><<<ceil_div(n, 256), 256, 0, s>>>(indptr, col, val, n, labels, f_far, f_unk,
+                                                                   cnt.as<int32_t>(), nullptr, nullptr, nullptr);
+    UMAP_LAUNCH_CHECK("supervised_rows_kernel<count>");
+    UMAP_TRY(exclusive_scan<int32_t>(cnt.as<int32_t>(), n, out_indptr, s));
+    int64_t total = 0;
+    UMAP_CUDA_TRY(cudaMemcpyAsync(&total, out_indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    if (total > capacity) {
+        set_last_error("supervised_adjust: capacity " + std::to_string(capacity) + " < nnz " + std::to_string(total));
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    supervised_rows_kernel<true><<<ceil_div(n, 256), 256, 0, s>>>(indptr, col, val, n, labels, f_far, f_unk, nullptr,
+                                                                  out_indptr, out_col, out_val);
+    UMAP_LAUNCH_CHECK("supervised_rows_kernel<fill>");
     if (nnz_host) *nnz_host = total;
     return UMAP_OK;
 }

@@ -480,3 +480,28 @@ def test_c5_transform_chunk_sampled_rows(O):
     for r in (0, 123457, 999999):
         yo = O.transform(Xtr, Ytr_h, np_(Xq[r:r + 1]), k=15, n_epochs=200, a=A_, b=B_, seed=0, q_offset=3000000 + r)
         assert np.abs(np_(Yq[r]) - yo[0]).max() < 1e-3
+
+
+# ------------------------------------------------------------------- supervised (f4, R17)
+def test_supervised_adjust_bitexact(O):
+    X = synth.lowrank(1500, 16, blobs=4, seed=21)
+    _, _, _, _, _, (indptr, col, w) = O.fuzzy_graph(X, 15)
+    lab = np.random.default_rng(4).integers(-1, 4, 1500).astype(np.int32)
+    for far, unk in [(5.0, 1.0), (40.0, 30.0), (0.0, 0.0)]:
+        ri, rc, rv = O.supervised_adjust(indptr, col, w, lab, far, unk)
+        gi, gc, gv = U.supervised_adjust(cu(indptr), cu(col), cu(w), cu(lab), far, unk)
+        assert np.array_equal(np_(gi), ri) and np.array_equal(np_(gc), rc) and np.array_equal(np_(gv), rv)
+
+
+def test_supervised_fit_c1_vs_oracle(O):
+    """Supervised fit at digits shape (labels = the blob ids, a quarter unknown): trust within
+    0.005 of the oracle's supervised fit."""
+    X, lab = synth.lowrank(1797, 64, blobs=10, seed=0, return_labels=True)
+    lab = lab.astype(np.int32)
+    lab[np.random.default_rng(1).random(1797) < 0.25] = -1
+    Y, st = U.fit(cu(X), labels=torch.from_numpy(lab), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=1,
+                  trust_k=15)
+    Yr = O.fit(X, k=15, n_epochs=200, a=A_, b=B_, seed=1, mode="deterministic", labels=lab)
+    assert abs(st["trustworthiness"] - O.trustworthiness(X, Yr, 15)) < 0.005
+    Y0, st0 = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=1)
+    assert st["nnz"] <= st0["nnz"]
