@@ -162,6 +162,71 @@ def random_init(n: int, dim: int, seed: int):
     return Y
 
 
+def philox_vec(c0, c1, c2, c3, seed: int):
+    """Philox4x32-10 (R11) vectorised over numpy uint32 counter arrays (same rounds as the C
+    oracle; pinned against it by tests/test_oracle.py)."""
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    W0, W1 = 0x9E3779B9, 0xBB67AE85
+    c0, c1, c2, c3 = (np.asarray(x, np.uint64) & np.uint64(0xFFFFFFFF) for x in (c0, c1, c2, c3))
+    k0, k1 = seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF
+    mask = np.uint64(0xFFFFFFFF)
+    for r in range(10):
+        if r:
+            k0, k1 = (k0 + W0) & 0xFFFFFFFF, (k1 + W1) & 0xFFFFFFFF
+        p0, p1 = M0 * c0, M1 * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & mask
+        hi1, lo1 = p1 >> np.uint64(32), p1 & mask
+        c0, c1, c2, c3 = hi1 ^ c1 ^ np.uint64(k0), lo1, hi0 ^ c3 ^ np.uint64(k1), lo0
+    return c0.astype(np.uint32), c1.astype(np.uint32), c2.astype(np.uint32), c3.astype(np.uint32)
+
+
+def _uniform_pm1(n, dim, seed, tag):
+    """U[-1, 1) per (row, column) from Philox counter (row, column, tag, 0), first word."""
+    i = np.repeat(np.arange(n, dtype=np.uint64), dim)
+    c = np.tile(np.arange(dim, dtype=np.uint64), n)
+    u = philox_vec(i, c, np.full(i.shape, tag, np.uint64), np.zeros(i.shape, np.uint64), seed)[0]
+    return (-1.0 + 2.0 * (u >> np.uint32(8)).astype(np.float64) * 2.0 ** -24).reshape(n, dim)
+
+
+def spectral_init(indptr, col, w, dim, seed=0, iters=300, scale=10.0):
+    """Spectral initialisation ("computing a spectral embedding over the fuzzy union",
+    P:134; reading R18): the dim eigenvectors of L = I - D^-1/2 B D^-1/2 with the
+    smallest non-trivial eigenvalues, by orthogonal (block power) iteration on
+    M = 2I - L = I + D^-1/2 B D^-1/2 with the trivial vector D^1/2 1 deflated, in fp64:
+    V0 = U[-1,1) from Philox (row, column, 0xFFFFFFFE); `iters` times W = M V, W -= v0 (v0' W),
+    V = W R^-1 with R'R = W'W (Cholesky QR).  Each column is then rescaled affinely to
+    [-scale, scale] and noise 1e-4 scale U[-1,1) (counter tag 0xFFFFFFFD) is added; fp32 out."""
+    indptr, col = np.asarray(indptr, np.int64), np.asarray(col, np.int64)
+    w = np.asarray(w, np.float32).astype(np.float64)
+    n = indptr.shape[0] - 1
+    rows = np.repeat(np.arange(n), np.diff(indptr))
+    deg = np.zeros(n)
+    for i in range(n):  # row sums in CSR order (sequential, as the definition reads)
+        s_ = 0.0
+        for e in range(indptr[i], indptr[i + 1]):
+            s_ += w[e]
+        deg[i] = s_
+    sq = np.sqrt(deg)
+    dinv = np.where(sq > 0, 1.0 / np.where(sq > 0, sq, 1.0), 0.0)
+    v0 = sq / np.linalg.norm(sq)
+    V = _uniform_pm1(n, dim, seed, 0xFFFFFFFE)
+    for _ in range(iters):
+        Z = dinv[:, None] * V
+        BZ = np.zeros_like(V)
+        np.add.at(BZ, rows, w[:, None] * Z[col])
+        W_ = V + dinv[:, None] * BZ
+        d0 = v0 @ W_
+        W_ = W_ - np.outer(v0, d0)
+        G = W_.T @ W_
+        R = np.linalg.cholesky(G).T
+        V = W_ @ np.linalg.inv(R)
+    lo, hi = V.min(0), V.max(0)
+    span = np.where(hi > lo, hi - lo, 1.0)
+    Y = (V - lo) / span * (2.0 * scale) - scale
+    Y = Y + 1e-4 * scale * _uniform_pm1(n, dim, seed, 0xFFFFFFFD)
+    return Y.astype(np.float32), V
+
+
 def edge_due(r: float, e: int) -> bool:
     return bool(lib().oracle_edge_due(np.float32(r), e))
 
@@ -268,7 +333,7 @@ def supervised_adjust(indptr, col, w, labels, far_dist=5.0, unknown_dist=1.0):
 
 
 def fit(X, k=15, n_components=2, n_epochs=None, a=None, b=None, min_dist=0.1, spread=1.0, m=5, seed=0,
-        mode="deterministic", labels=None, far_dist=5.0, unknown_dist=1.0):
+        mode="deterministic", labels=None, far_dist=5.0, unknown_dist=1.0, init="random", spectral_iters=300):
     """Whole fit: kNN -> rho/sigma -> membership -> union -> (labels: supervised adjustment)
     -> init -> SGD (P:47-61, P:77, P:97-140)."""
     X = _f32(X)
@@ -280,7 +345,10 @@ def fit(X, k=15, n_components=2, n_epochs=None, a=None, b=None, min_dist=0.1, sp
     _, _, _, _, _, (indptr, col, w) = fuzzy_graph(X, k)
     if labels is not None:
         indptr, col, w = supervised_adjust(indptr, col, w, labels, far_dist, unknown_dist)
-    Y0 = random_init(n, n_components, seed)
+    if init == "spectral":
+        Y0, _ = spectral_init(indptr, col, w, n_components, seed, spectral_iters)
+    else:
+        Y0 = random_init(n, n_components, seed)
     return optimize(indptr, col, w, Y0, np.float32(a), np.float32(b), n_epochs, m=m, seed=seed, mode=mode)
 
 

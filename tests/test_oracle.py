@@ -424,3 +424,71 @@ def test_supervised_adjust_properties():
     assert abs(B - B.T).max() == 0
     p, c, v = O.supervised_adjust(indptr, col, w, np.arange(300), far_dist=40.0)
     assert v.size < w.size and (v >= 1e-8).all()
+
+
+# ------------------------------------------------------------------- spectral init (f3, R18)
+def _csr(n, edges):
+    import scipy.sparse as sp
+    r = [a for a, b, _ in edges] + [b for a, b, _ in edges]
+    c = [b for a, b, _ in edges] + [a for a, b, _ in edges]
+    v = [x for _, _, x in edges] * 2
+    B = sp.csr_matrix((np.array(v, np.float32), (r, c)), shape=(n, n))
+    B.sort_indices()
+    return B.indptr.astype(np.int64), B.indices.astype(np.int32), B.data.astype(np.float32), B
+
+
+def test_philox_vec_matches_c_oracle():
+    from oracle import oracle as O
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2**32, (50, 4), dtype=np.uint64)
+    seed = int(rng.integers(0, 2**63))
+    v = O.philox_vec(ctr[:, 0], ctr[:, 1], ctr[:, 2], ctr[:, 3], seed)
+    for i in range(50):
+        ref = O.philox4x32_10(ctr[i].astype(np.uint32), np.array([seed & 0xFFFFFFFF, seed >> 32], np.uint32))
+        assert [int(x[i]) for x in v] == [int(x) for x in ref]
+
+
+def test_spectral_init_spec_examples():
+    """two disconnected 3-cliques -> the first non-trivial coordinate separates them
+    by sign; 3-node path with unit weights -> non-trivial eigenvector prop. to (-1, 0, 1)."""
+    from oracle import oracle as O
+    edges = [(0, 1, 1.0), (0, 2, 1.0), (1, 2, 1.0), (3, 4, 1.0), (3, 5, 1.0), (4, 5, 1.0)]
+    ip, c, w, _ = _csr(6, edges)
+    Y, V = O.spectral_init(ip, c, w, 1, seed=3, iters=200)
+    assert np.sign(V[0, 0]) == np.sign(V[1, 0]) == np.sign(V[2, 0]) != np.sign(V[3, 0])
+    assert np.sign(V[3, 0]) == np.sign(V[4, 0]) == np.sign(V[5, 0])
+    ip, c, w, _ = _csr(3, [(0, 1, 1.0), (1, 2, 1.0)])
+    Y, V = O.spectral_init(ip, c, w, 1, seed=1, iters=200)
+    assert abs(V[1, 0]) < 1e-8 and abs(V[0, 0] + V[2, 0]) < 1e-8
+    assert np.abs(np.abs(Y[:, 0]) - np.array([10, 0, 10])).max() < 2e-3  # rescaled to [-10, 10] + noise
+
+
+def test_spectral_init_matches_dense_eigensolver():
+    """Three weakly linked clusters: after the iterations the 2-D subspace equals the dense
+    eigensolver's (eigenvalues 2 and 3 of L = I - D^-1/2 B D^-1/2), V is orthogonal to the
+    trivial vector D^1/2 1, and each column satisfies the residual bound |L v - l v| <= 1e-3 |v|."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(2)
+    edges = []
+    for g in range(3):
+        base = 20 * g
+        for i in range(20):
+            for j in range(i + 1, 20):
+                if rng.random() < 0.5:
+                    edges.append((base + i, base + j, float(rng.uniform(0.3, 1.0))))
+    edges += [(0, 20, 0.01), (20, 40, 0.01), (40, 1, 0.01)]
+    ip, c, w, B = _csr(60, edges)
+    Y, V = O.spectral_init(ip, c, w, 2, seed=7, iters=500)
+    deg = np.asarray(B.astype(np.float64).sum(1)).ravel()
+    Dm = np.diag(1 / np.sqrt(deg))
+    L = np.eye(60) - Dm @ B.toarray().astype(np.float64) @ Dm
+    lam, U = np.linalg.eigh(L)
+    Q = U[:, 1:3]
+    s = np.linalg.svd(Q.T @ V, compute_uv=False)  # cosines of the principal angles
+    assert s.min() > 1 - 1e-8
+    v0 = np.sqrt(deg) / np.linalg.norm(np.sqrt(deg))
+    assert np.abs(v0 @ V).max() < 1e-10
+    for j in range(2):
+        v = V[:, j]
+        lj = v @ L @ v / (v @ v)
+        assert np.linalg.norm(L @ v - lj * v) <= 1e-3 * np.linalg.norm(v)
