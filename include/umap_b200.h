@@ -89,6 +89,8 @@ typedef struct {
     float    far_dist;             /* supervised (umap_fit_supervised): different labels ->  */
                                    /* weight x exp(-far_dist), default 5.0 (R17)             */
     float    unknown_dist;         /* a label -1 on either end -> x exp(-unknown_dist), 1.0  */
+    int32_t  init;                 /* a7: 0 = random U[-10,10) (R11), 1 = spectral (R18)     */
+    int32_t  spectral_iters;       /* block power iterations of the spectral init, 0 -> 300  */
 } umap_params;
 
 /* Per-stage device times (ms, CUDA events on `stream`) and graph statistics. */
@@ -219,6 +221,14 @@ UMAP_API umap_status umap_transform_optimize(const int32_t* idx, const float* w,
  * exp(-p->unknown_dist) (either unknown), entries below 1e-8 dropped. */
 UMAP_API umap_status umap_fit_supervised(const float* X, int64_t n, int32_t d, const int32_t* labels,
                                          const umap_params* p, float* Y, umap_fit_stats* stats, void* stream);
+
+/* Spectral initialisation (f3, R18) of a device CSR graph B (symmetric, n+1
+ * int64 indptr, int32 col, fp32 val): the n_components eigenvectors of
+ * L = I - D^-1/2 B D^-1/2 with the smallest non-trivial eigenvalues by `iters` fp64 block
+ * power iterations on 2I - L (trivial vector deflated), columns rescaled to [-10, 10] plus
+ * 1e-3 Philox noise.  Y: device n x dim fp32.  dim in {1,2,3,4,8,16}, n >= dim + 2. */
+UMAP_API umap_status umap_spectral_init(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
+                                        int32_t dim, uint64_t seed, int32_t iters, float* Y, void* stream);
 
 /* The label adjustment alone on a device CSR (indptr n+1 int64, col int32, val fp32): writes
  * the adjusted CSR (out_indptr n+1, out_col / out_val with room for `capacity` entries) and

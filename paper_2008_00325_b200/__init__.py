@@ -8,9 +8,9 @@ from .api import (fit, fit_ab, fit_knn, fuzzy_union, kernel_launch_count, knn, o
                   topk_merge, transform, transform_optimize, trust_from_penalty, trust_penalty, trustworthiness,
                   version, default_transform_epochs, trust_ambiguous_count,
                   profile_begin, profile_end, trust_fine_fraction,
-                  supervised_adjust)
+                  supervised_adjust, spectral_init)
 
 __all__ = ["fit", "fit_ab", "fit_knn", "fuzzy_union", "kernel_launch_count", "knn", "optimize", "params", "random_init",
            "smooth_knn", "topk_merge", "transform", "transform_optimize", "trust_from_penalty", "trust_penalty",
            "trustworthiness", "version", "default_transform_epochs", "trust_ambiguous_count", "profile_begin", "profile_end", "trust_fine_fraction",
-           "supervised_adjust"]
+           "supervised_adjust", "spectral_init"]

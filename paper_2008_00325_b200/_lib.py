@@ -30,7 +30,7 @@ class UmapParams(ctypes.Structure):
                 ("negative_sample_rate", c_int32), ("learning_rate", c_float), ("repulsion_strength", c_float),
                 ("a", c_float), ("b", c_float), ("seed", c_uint64), ("sgd_mode", c_int32), ("knn_mode", c_int32),
                 ("knn_candidates", c_int32), ("transform_epochs", c_int32), ("trust_k", c_int32),
-                ("far_dist", c_float), ("unknown_dist", c_float)]
+                ("far_dist", c_float), ("unknown_dist", c_float), ("init", c_int32), ("spectral_iters", c_int32)]
 
 
 class UmapFitStats(ctypes.Structure):
@@ -53,6 +53,8 @@ SIGNATURES = {
                                       P(UmapFitStats), c_void_p]),
     "umap_supervised_adjust": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_float, c_float,
                                          c_void_p, c_void_p, c_void_p, c_int64, P(c_int64), c_void_p]),
+    "umap_spectral_init": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_uint64, c_int32, c_void_p,
+                                     c_void_p]),
     "umap_fit_knn": (c_int32, [c_void_p, c_void_p, c_int64, P(UmapParams), c_void_p, P(UmapFitStats), c_void_p]),
     "umap_transform": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_int64, P(UmapParams),
                                  c_void_p, c_void_p]),

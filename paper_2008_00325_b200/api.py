@@ -44,7 +44,7 @@ def _any(t, dtype, name):
 def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0, negative_sample_rate=5,
            learning_rate=1.0, repulsion_strength=1.0, a=0.0, b=0.0, seed=0, sgd_mode="deterministic",
            knn_mode="exact", knn_candidates=32, transform_epochs=0, trust_k=0, far_dist=5.0,
-           unknown_dist=1.0) -> UmapParams:
+           unknown_dist=1.0, init="random", spectral_iters=0) -> UmapParams:
     p = UmapParams()
     _lib.load().umap_params_default(ctypes.byref(p))
     p.n_neighbors, p.n_components, p.n_epochs = n_neighbors, n_components, n_epochs
@@ -55,6 +55,8 @@ def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0,
     p.knn_mode = KNN_MODES[knn_mode] if isinstance(knn_mode, str) else knn_mode
     p.knn_candidates, p.transform_epochs, p.trust_k = knn_candidates, transform_epochs, trust_k
     p.far_dist, p.unknown_dist = far_dist, unknown_dist
+    p.init = {"random": 0, "spectral": 1}[init] if isinstance(init, str) else init
+    p.spectral_iters = spectral_iters
     return p
 
 
@@ -85,6 +87,18 @@ def fit(X, out=None, labels=None, **kw):
         check(_lib.load().umap_fit_supervised(_ptr(X), n, d, _ptr(labels), ctypes.byref(p), _ptr(out),
                                               ctypes.byref(st), _stream(dev)), "umap_fit_supervised")
     return out, st.as_dict()
+
+
+def spectral_init(indptr, col, val, dim=2, seed=0, iters=300):
+    """umap_spectral_init on a device CSR graph -> Y (n x dim fp32, device)."""
+    indptr = _dev(indptr, torch.int64, "indptr")
+    col = _dev(col, torch.int32, "col")
+    val = _dev(val, torch.float32, "val")
+    n = indptr.shape[0] - 1
+    Y = torch.empty((n, dim), dtype=torch.float32, device=indptr.device)
+    check(_lib.load().umap_spectral_init(_ptr(indptr), _ptr(col), _ptr(val), n, dim, seed, iters, _ptr(Y),
+                                         _stream(indptr.device)), "umap_spectral_init")
+    return Y
 
 
 def supervised_adjust(indptr, col, val, labels, far_dist=5.0, unknown_dist=1.0):

@@ -35,6 +35,8 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
                           int64_t row_end, int64_t* row_pen, int64_t* penalty_host, int knn_mode, const float* Y,
                           int d_emb, cudaStream_t s);
 bool dim_supported(int dim);
+umap_status spectral_init(const int64_t* indptr, const int32_t* col, const float* val, int64_t n, int dim,
+                          uint64_t seed, int iters, float* Y, cudaStream_t s);
 umap_status supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,
                               const int32_t* labels, float far_dist, float unknown_dist, int64_t* out_indptr,
                               int32_t* out_col, float* out_val, int64_t capacity, int64_t* nnz_host, cudaStream_t s);
@@ -57,7 +59,7 @@ static const char* const k_prof_names[PROF_NSLOTS] = {
     "knn_tc_kernel (kNN candidates)", "rerank_kernel", "knn_tc_kernel (trust ranks)", "rank_fix_kernel",
     "thresholds_warp_kernel", "grid_knn_kernel", "smooth_knn_kernel", "fuzzy union (5 kernels)",
     "sgd_persistent_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
-    "transform_sgd_kernel", "knn_tc_kernel (trust coarse)"};
+    "transform_sgd_kernel", "knn_tc_kernel (trust coarse)", "spectral init (3 kernels x iterations)"};
 void count_launch(int n) { g_launches += n; }
 
 umap_status cuda_status(cudaError_t e, const char* what)
@@ -212,6 +214,10 @@ umap_status check_params(const umap_params* p)
         set_last_error("unknown knn_mode");
         return UMAP_ERR_INVALID_ARGUMENT;
     }
+    if (p->init != 0 && p->init != 1) {
+        set_last_error("init must be 0 (random) or 1 (spectral)");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
     return UMAP_OK;
 }
 
@@ -330,6 +336,8 @@ void umap_params_default(umap_params* p)
     p->trust_k = 0;
     p->far_dist = 5.0f;
     p->unknown_dist = 1.0f;
+    p->init = 0;
+    p->spectral_iters = 0;
 }
 
 // R8: Levenberg-Marquardt least squares of Phi(x) = 1/(1 + a x^{2b}) against the
@@ -591,8 +599,12 @@ umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const
         g_val = sval.as<float>();
     }
     st.ms_union = tm.lap();
-    // a7
-    UMAP_TRY(random_init(n, dim, p.seed, Yd, s));
+    // a7 (random, R11, or spectral on the graph the SGD uses, R18)
+    if (p.init == 1)
+        UMAP_TRY(spectral_init(g_indptr, g_col, g_val, n, dim, p.seed, p.spectral_iters > 0 ? p.spectral_iters : 300,
+                               Yd, s));
+    else
+        UMAP_TRY(random_init(n, dim, p.seed, Yd, s));
     st.ms_init = tm.lap();
     // a6 + a8
     int64_t positives = 0;
@@ -629,6 +641,24 @@ umap_status umap_fit_supervised(const float* X, int64_t n, int32_t d, const int3
 {
     if (!labels) { set_last_error("labels required"); return UMAP_ERR_INVALID_ARGUMENT; }
     return fit_impl(X, n, d, labels, p, Y, stats, stream);
+}
+
+umap_status umap_spectral_init(const int64_t* indptr, const int32_t* col, const float* val, int64_t n, int32_t dim,
+                               uint64_t seed, int32_t iters, float* Y, void* stream)
+{
+    UMAP_TRY(require_cuda());
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!dim_supported(dim) || iters < 0 || !indptr || !col || !val || !Y) {
+        set_last_error("spectral_init: dim in {1,2,3,4,8,16}, iters >= 0, arrays required");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    UMAP_TRY(require_device(indptr, "indptr"));
+    UMAP_TRY(require_device(col, "col"));
+    UMAP_TRY(require_device(val, "val"));
+    UMAP_TRY(require_device(Y, "Y"));
+    UMAP_TRY(spectral_init(indptr, col, val, n, dim, seed, iters, Y, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    return UMAP_OK;
 }
 
 umap_status umap_supervised_adjust(const int64_t* indptr, const int32_t* col, const float* val, int64_t n,

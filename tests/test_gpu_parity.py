@@ -505,3 +505,20 @@ def test_supervised_fit_c1_vs_oracle(O):
     assert abs(st["trustworthiness"] - O.trustworthiness(X, Yr, 15)) < 0.005
     Y0, st0 = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=1)
     assert st["nnz"] <= st0["nnz"]
+
+
+# ------------------------------------------------------------------- spectral init (f3, R18)
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_spectral_init_vs_oracle(O, dim):
+    X = synth.lowrank(1797, 64, blobs=10, seed=0)
+    _, _, _, _, _, (indptr, col, w) = O.fuzzy_graph(X, 15)
+    Yr, _ = O.spectral_init(indptr, col, w, dim, seed=5, iters=300)
+    Yg = U.spectral_init(cu(indptr), cu(col), cu(w), dim, seed=5, iters=300)
+    assert np.abs(np_(Yg) - Yr).max() < 1e-3
+
+
+def test_spectral_fit_c1_vs_oracle(O):
+    X = synth.lowrank(1797, 64, blobs=10, seed=0)
+    Y, st = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=1, init="spectral", trust_k=15)
+    Yr = O.fit(X, k=15, n_epochs=200, a=A_, b=B_, seed=1, mode="deterministic", init="spectral")
+    assert abs(st["trustworthiness"] - O.trustworthiness(X, Yr, 15)) < 0.005
