@@ -7,7 +7,14 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
 Wraps ``oracle/liboracle.so`` (plain C, see ``umap_oracle.c``) with numpy, plus
 the a/b curve fit (R8) done with scipy's Levenberg-Marquardt ``curve_fit`` on the
 fixed 300-point grid.  Every function cites the passage it follows; the readings
-R1..R16 are listed in DESIGN.md.
+R1..R18 are listed in DESIGN.md.
+
+Parity unpinned (no value in the paper to pin them to; they are fixed only by the readings
+and checked through invariants): the self-exclusion convention of knn (R1), the bracket and
+tolerance of smooth_knn's bisection (R5), the closed-form schedule of optimize (R9), the
+Philox stream of random_init / negative samples (R11), the s = 0 repulsion kick (R12), the
+transform epoch budget (R15), spectral_init's iteration count (R18), and Hogwild
+trajectories (optimize mode="hogwild", compared only through trustworthiness).
 """
 from __future__ import annotations
 
