@@ -522,3 +522,28 @@ def test_spectral_fit_c1_vs_oracle(O):
     Y, st = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=1, init="spectral", trust_k=15)
     Yr = O.fit(X, k=15, n_epochs=200, a=A_, b=B_, seed=1, mode="deterministic", init="spectral")
     assert abs(st["trustworthiness"] - O.trustworthiness(X, Yr, 15)) < 0.005
+
+
+def test_spectral_and_supervised_edge_cases(O):
+    """Isolated vertices (degree 0) in the spectral init; all labels unknown (-1) and all
+    labels distinct with a far_dist that drops every edge in the supervised adjustment."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(9)
+    n = 300
+    r = rng.integers(0, n - 10, 2000)
+    c = rng.integers(0, n - 10, 2000)
+    keep = r != c
+    W = sp.coo_matrix((rng.uniform(0.1, 1, keep.sum()).astype(np.float32), (r[keep], c[keep])), shape=(n, n)).tocsr()
+    W = ((W + W.T) * 0.5).tocsr()
+    W.sort_indices()
+    ip, cl, w = W.indptr.astype(np.int64), W.indices.astype(np.int32), W.data.astype(np.float32)
+    Yr, _ = O.spectral_init(ip, cl, w, 2, seed=2, iters=300)
+    Yg = U.spectral_init(cu(ip), cu(cl), cu(w), 2, seed=2, iters=300)
+    assert np.abs(np_(Yg) - Yr).max() < 1e-3          # the last 10 rows are isolated
+    lab = np.full(n, -1, np.int32)
+    gi, gc, gv = U.supervised_adjust(cu(ip), cu(cl), cu(w), cu(lab), 5.0, 1.0)
+    ri, rc, rv = O.supervised_adjust(ip, cl, w, lab, 5.0, 1.0)
+    assert np.array_equal(np_(gi), ri) and np.array_equal(np_(gv), rv)
+    lab = np.arange(n, dtype=np.int32)
+    gi, gc, gv = U.supervised_adjust(cu(ip), cu(cl), cu(w), cu(lab), 80.0, 1.0)
+    assert gc.numel() == 0 and int(np_(gi)[-1]) == 0
