@@ -8,6 +8,8 @@
 // enter the top-k is examined, so the result is bit-identical to the brute-force
 // definition.  The lower bound is taken one ring early to absorb rounding in the cell
 // assignment.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace umapb200 {
@@ -217,8 +219,24 @@ __device__ __forceinline__ uint32_t spread16(uint32_t v)
     return v;
 }
 
+// Hilbert index of (x, y) on a 2^16 x 2^16 grid (the classic rotate-and-flip walk): unlike the
+// Z order it has no long jumps, so consecutive rows stay inside one 2-D region longer
+__device__ __forceinline__ uint32_t hilbert16(uint32_t x, uint32_t y)
+{
+    uint32_t d = 0;
+    for (uint32_t s = 1u << 15; s > 0; s >>= 1) {
+        const uint32_t rx = (x & s) > 0, ry = (y & s) > 0;
+        d += s * s * ((3 * rx) ^ ry);
+        if (ry == 0) {
+            if (rx == 1) { x = s - 1 - x; y = s - 1 - y; }
+            const uint32_t t = x; x = y; y = t;
+        }
+    }
+    return d;
+}
+
 __global__ void morton_kernel(const float* __restrict__ Y, int64_t n, const float* __restrict__ box,
-                              uint32_t* __restrict__ keys, int32_t* __restrict__ vals)
+                              uint32_t* __restrict__ keys, int32_t* __restrict__ vals, int hilbert)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -226,7 +244,7 @@ __global__ void morton_kernel(const float* __restrict__ Y, int64_t n, const floa
     const float2 p = reinterpret_cast<const float2*>(Y)[i];
     const uint32_t cx = (uint32_t)cell_coord(p.x, g.x0, g.inv_h, 65536);
     const uint32_t cy = (uint32_t)cell_coord(p.y, g.y0, g.inv_h, 65536);
-    keys[i] = spread16(cx) | (spread16(cy) << 1);
+    keys[i] = hilbert ? hilbert16(cx, cy) : (spread16(cx) | (spread16(cy) << 1));
     vals[i] = (int32_t)i;
 }
 
@@ -261,7 +279,8 @@ umap_status cluster_order(const float* Y, int64_t n, int d_emb, int32_t* perm, c
     bbox_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4LL * num_sms()), 256, 0, s>>>(Y, n, box.as<float>());
     UMAP_LAUNCH_CHECK("bbox_kernel");
     UMAP_TRY(keys.alloc(sizeof(uint32_t) * (size_t)n, s));
-    morton_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Y, n, box.as<float>(), keys.as<uint32_t>(), perm);
+    const int hilbert = getenv("UMAP_ORDER_MORTON") ? 0 : 1;  // A/B knob
+    morton_kernel<<<ceil_div(n, 256), 256, 0, s>>>(Y, n, box.as<float>(), keys.as<uint32_t>(), perm, hilbert);
     UMAP_LAUNCH_CHECK("morton_kernel");
     return sort_pairs_u32(keys.as<uint32_t>(), perm, n, s);
 }
