@@ -241,7 +241,7 @@ UMAP_API umap_status umap_supervised_adjust(const int64_t* indptr, const int32_t
 /* a10 input-space rank penalties for rows [row_begin, row_end) (R16): emb_idx is the
  * embedding kNN of those rows (n_rows x k, global ids).  knn_mode as in
  * umap_trustworthiness.  Y (optional, device, n x d_emb; NULL to omit) is the embedding:
- * with d_emb == 2 the tensor-core path visits rows and columns in the Morton order of Y
+ * with d_emb == 2 the tensor-core path visits rows and columns in the Hilbert order of Y
  * (a layout choice only: the integer result is the same).  row_pen: n_rows int64
  * (optional NULL); *penalty (host) = sum. */
 UMAP_API umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,

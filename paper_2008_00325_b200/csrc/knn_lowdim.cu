@@ -201,7 +201,7 @@ umap_status knn_grid2d(const float* Y, int64_t n, int k, int out_squared, int32_
 }  // namespace umapb200
 
 // ---------------------------------------------------------------- cluster order of an embedding
-// Morton (Z-order) key of each 2-D point on a 2^16 x 2^16 grid over the bounding box, then a
+// Hilbert (default) or Morton (Z-order, UMAP_ORDER_MORTON) key of each 2-D point on a 2^16 x 2^16 grid over the bounding box, then a
 // stable radix sort of (key, row): perm[p] = the row at position p.  Used by the trust path
 // to visit rows and columns cluster by cluster (a layout choice; results do not depend on it).
 #include <cub/device/device_radix_sort.cuh>

@@ -1258,7 +1258,7 @@ umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_
 // rows [row_begin, row_end) of X, references = all of X.  Exact thresholds in, exact
 // non-cumulative bucket counts out (hist [rows][k]); the approximate pass only decides
 // pairs whose bucket is certain under the error bound, the rest are re-checked exactly.
-// Y (optional, n x 2): the embedding; rows and columns are then processed in the Morton
+// Y (optional, n x 2): the embedding; rows and columns are then processed in the Hilbert
 // order of Y (counts do not depend on the order), which groups each query block with the
 // reference tiles of its own cluster: most column chunks then hold no candidate for any
 // row of a warp, and the others hold candidates for all of them.
