@@ -328,6 +328,7 @@ def run_ours(args):
         # N > 1: every rank stages the (replicated) pinned host X itself, runs the sharded step
         # and reads its result back; wall clock between barriers, max over ranks
         e2e_ms = []
+        step(X_host.to("cuda", non_blocking=True))  # untimed: grows the memory pools for the staged copy
         for i in range(max(1, min(args.steps, 3))):
             flush.fill_(float(i))
             barrier()
@@ -346,6 +347,9 @@ def run_ours(args):
     if not args.no_e2e and world == 1:
         e2e_ms = []
         Y_host = torch.empty((n, 2), dtype=torch.float32, pin_memory=True)
+        # one untimed call first: it grows the device memory pool for the staged X copy
+        # (the timed device steps above ran on an X that was already resident)
+        U.fit(X_host, out=Y_host, trust_k=trust_k, **kw)
         for i in range(max(1, min(args.steps, 3))):
             flush.fill_(float(i))
             barrier()
@@ -355,7 +359,8 @@ def run_ours(args):
         em = sum(e2e_ms) / len(e2e_ms)
         e2e = {"value": em / 1e3, "unit": "s", "h2d_bytes_per_step": int(X_host.numel() * 4),
                "d2h_bytes_per_step": int(Y_host.numel() * 4 + 8 + 8), "api": "umap_fit(X host, Y host, trust_k=15)",
-               "timer": "host wall clock around the synchronous call"}
+               "timer": "host wall clock around the synchronous call, after one untimed call",
+               "calls_ms": [round(x, 2) for x in e2e_ms]}
     clk = clocks.stop()
 
     if rank != 0:
