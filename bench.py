@@ -131,7 +131,7 @@ def profile_traffic(slot):
     summary, or None."""
     import glob
     want = NCU_NAME.get(slot)
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*.json")))  # ncu_r01a < ncu_r01b < ... (round tags)
     if not want or not files:
         return None, None
     try:
