@@ -39,6 +39,9 @@ struct SgdArgs {
     unsigned long long* positives;  // device counter of due directed edges
     unsigned int* bar;       // grid barrier counters (BAR_WORDS words)
     const uint8_t* owner;    // per CSR entry: head vertex & 255 (its lane in the owning chunk)
+    const uint16_t* hoff;    // flat kernel: per CSR entry, head vertex - first vertex of its piece
+    int64_t nnz;
+    int32_t vt;              // flat kernel: piece size (vertices whose sums are held in shared memory)
     int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only
 };
 
@@ -355,6 +358,131 @@ __global__ void __launch_bounds__(32 * sgd_warps<MINB>(), MINB) sgd_persistent_k
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
 }
 
+// Deterministic SGD with the CTA's records split evenly over its warps.  CTA b owns the
+// vertex range [bounds[b], bounds[b+1]) (cost-balanced) and works through it in pieces of
+// at most vt vertices.  Within a piece the 32-record steps of the piece's CSR range go to
+// the warps round-robin (step s -> warp s mod W), so every warp gets ~1/W of the piece's
+// records whatever the degree mix (the chunk kernel above hands out whole 16-vertex chunks,
+// about one per warp per epoch at C2, and its warps idle at the CTA barrier).  Head sums:
+// warp-segmented int sums as above, then one 64-bit shared atomic per segment into the
+// piece's fixed-point accumulators; integer addition is associative, so the result is
+// bit-identical to the chunk kernel's whatever the order (R13).
+template <int DIM, int MC>
+__global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
+{
+    constexpr int W = 32;
+    extern __shared__ __align__(16) unsigned char sgd_smem[];
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(sgd_smem);  // [DIM][vt]
+    int32_t* const qh = reinterpret_cast<int32_t*>(acc + (size_t)DIM * A.vt) + (threadIdx.x >> 5) * QCAP;
+    int32_t* const qt = qh + W * QCAP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int vt = A.vt;
+    const int v_lo = A.bounds[blockIdx.x], v_hi = A.bounds[blockIdx.x + 1];
+    unsigned long long due_count = 0;
+    for (int epoch = A.e_begin; epoch < A.e_end; ++epoch) {
+        const int par = (epoch - A.e_begin) & 1;
+        const float* Yr = par ? A.Y1 : A.Y0;
+        float* Yw = par ? A.Y0 : A.Y1;
+        const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
+        const float ef = (float)epoch, ef1 = (float)(epoch - 1);
+        for (int pv0 = v_lo; pv0 < v_hi; pv0 += vt) {
+            const int np = min(vt, v_hi - pv0);
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) acc[c * vt + i] = 0ull;
+            }
+            __syncthreads();
+            const int64_t E0 = __ldg(A.indptr + pv0), E1 = __ldg(A.indptr + pv0 + np);
+            int qn = 0;
+            auto drain = [&](int count) {
+                const bool act = lane < count;
+                const int hl = act ? qh[lane] : -1;
+                int qa[DIM];
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) qa[c] = 0;
+                if (act) process_edge<DIM, true, MC>(A, Yr, Yw, epoch, alpha, pv0 + hl, qt[lane], qa);
+                long long sv[DIM];
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) sv[c] = qa[c];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int ho = __shfl_up_sync(0xffffffffu, hl, o);
+#pragma unroll
+                    for (int c = 0; c < DIM; ++c) {
+                        const long long so = __shfl_up_sync(0xffffffffu, sv[c], o);
+                        if (lane >= o && ho == hl) sv[c] += so;
+                    }
+                }
+                const int hn = __shfl_down_sync(0xffffffffu, hl, 1);
+                if (act && (lane == count - 1 || hn != hl)) {
+#pragma unroll
+                    for (int c = 0; c < DIM; ++c) atomicAdd(acc + c * vt + hl, (unsigned long long)sv[c]);
+                }
+                __syncwarp();
+            };
+            int64_t base = E0 + 32 * warp;
+            int2 nrec = make_int2(0, 0);
+            int nho = 0;
+            if (base + lane < E1) { nrec = __ldg(A.edges + base + lane); nho = __ldg(A.hoff + base + lane); }
+            for (; base < E1; base += 32 * W) {
+                const int64_t e = base + lane;
+                const int2 rec = nrec;  // records and head offsets prefetched one step ahead
+                const int ho = nho;
+                if (base + 32 * W + lane < E1) {
+                    nrec = __ldg(A.edges + base + 32 * W + lane);
+                    nho = __ldg(A.hoff + base + 32 * W + lane);
+                }
+                const bool due = e < E1 && edge_due_f(__int_as_float(rec.y), ef, ef1);
+                const unsigned ballot = __ballot_sync(0xffffffffu, due);
+                due_count += __popc(ballot);
+                if (due) {
+                    const int pos = qn + __popc(ballot & ((1u << lane) - 1u));
+                    qh[pos] = ho;
+                    qt[pos] = rec.x;
+                }
+                __syncwarp();
+                qn += __popc(ballot);
+                if (qn >= 32) {
+                    drain(32);
+                    qn -= 32;
+                    if (lane < qn) { qh[lane] = qh[32 + lane]; qt[lane] = qt[32 + lane]; }
+                    __syncwarp();
+                }
+            }
+            if (qn > 0) drain(qn);
+            __syncthreads();
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int v = pv0 + i;
+                float yo[DIM];
+                load_row<DIM>(Yr, v, yo);
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) {
+                    const double upd = (double)(long long)acc[c * vt + i] * (1.0 / 16777216.0);
+                    Yw[(int64_t)v * DIM + c] = (float)((double)yo[c] + upd);
+                }
+            }
+            __syncthreads();
+        }
+        if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1));
+    }
+    if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
+// per CSR entry: head vertex - first vertex of its piece (CTA ranges `bounds`, pieces of vt)
+__global__ void hoff_kernel(const int64_t* __restrict__ indptr, int64_t n, const int32_t* __restrict__ bounds, int G,
+                            int vt, uint16_t* __restrict__ hoff)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int lo = 0, hi = G - 1;  // last b with bounds[b] <= v
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (bounds[mid] <= v) lo = mid; else hi = mid - 1;
+    }
+    const uint16_t off = (uint16_t)((v - bounds[lo]) % vt);
+    for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) hoff[e] = off;
+}
+
 // Edge-balanced CTA ranges for the persistent SGD kernel: CTA b gets the chunks whose
 // cost prefix W(c) = indptr[c VPW] + 2 c VPW (edges + per-vertex work) starts in
 // [b W / G, (b + 1) W / G).  bounds[0] = 0, bounds[G] = n_chunks.
@@ -538,6 +666,37 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
     return UMAP_OK;
 }
 
+template <int DIM, int MC>
+umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
+{
+    auto kern = sgd_flat_kernel<DIM, MC>;
+    A.vt = std::min(4096, 65536 / (8 * DIM));
+    const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
+    static bool attr = false;
+    if (!attr) {
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    int per_sm = 0;
+    UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
+    const int grid = std::max(1, std::min(per_sm, 1) * num_sms());
+    A.n_chunks = A.n;
+    Scratch bounds, hoff;
+    UMAP_TRY(bounds.alloc(sizeof(int32_t) * (size_t)(grid + 1), s));
+    chunk_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(A.indptr, A.n, 1, (int)A.n, grid, bounds.as<int32_t>());
+    UMAP_LAUNCH_CHECK("chunk_bounds_kernel");
+    UMAP_TRY(hoff.alloc(sizeof(uint16_t) * (size_t)std::max<int64_t>(nnz, 1), s));
+    hoff_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.n, bounds.as<int32_t>(), grid, A.vt, hoff.as<uint16_t>());
+    UMAP_LAUNCH_CHECK("hoff_kernel");
+    A.bounds = bounds.as<int32_t>();
+    A.hoff = hoff.as<uint16_t>();
+    void* args[] = {&A};
+    ProfScope ps(PROF_SGD, s);
+    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(1024), args, smem, s));
+    UMAP_LAUNCH_CHECK("sgd_flat_kernel");
+    return UMAP_OK;
+}
+
 int sgd_variant()
 {
     static int v = -1;
@@ -579,6 +738,9 @@ umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
 template <int DIM>
 umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
 {
+    if (DIM <= 4 && det && sgd_variant() == 0) {  // DIM 8, 16: 64 registers per thread spill
+        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s) : launch_sgd_flat<DIM, 0>(A, A.nnz, s);
+    }
     if (A.m == 5) return det ? launch_sgd_m<DIM, true, 5>(A, s) : launch_sgd_m<DIM, false, 5>(A, s);
     return det ? launch_sgd_m<DIM, true, 0>(A, s) : launch_sgd_m<DIM, false, 0>(A, s);
 }
@@ -665,7 +827,7 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
         UMAP_TRY(other.alloc(sizeof(float) * (size_t)n * dim, s));
     }
     SgdArgs A{};
-    A.indptr = indptr; A.edges = edges.as<int2>(); A.n = n;
+    A.indptr = indptr; A.edges = edges.as<int2>(); A.n = n; A.nnz = nnz;
     A.Y0 = Y; A.Y1 = det ? other.as<float>() : Y;
     A.a = p->a; A.b = p->b; A.gamma = p->repulsion_strength; A.alpha0 = p->learning_rate;
     A.n_epochs = p->n_epochs; A.e_begin = e_begin; A.e_end = e_end; A.m = p->negative_sample_rate;
