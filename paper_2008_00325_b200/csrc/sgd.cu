@@ -23,6 +23,7 @@
 
 namespace umapb200 {
 
+template <class Tin> umap_status exclusive_scan(const Tin* in, int64_t n, int64_t* out, cudaStream_t s);  // graph.cu
 namespace {
 
 struct SgdArgs {
@@ -468,6 +469,35 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
 }
 
+// Expected per-epoch cost of vertex v's work in the flat kernel, in units of 1/256 record
+// scan: every record is scanned each epoch, record e is due in a fraction ~r_e of the epochs
+// (R9) and then costs cdue scans' worth (the gathers and the gradient), plus cvert for the
+// vertex's own read-modify-write.
+__global__ void vertex_cost_kernel(const int64_t* __restrict__ indptr, const int2* __restrict__ edges, int64_t n,
+                                   int cdue, int cvert, int64_t* __restrict__ cost)
+{
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int64_t c = 256LL * cvert;
+    for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e)
+        c += 256 + (int64_t)(256.0f * (float)cdue * __int_as_float(edges[e].y));
+    cost[v] = c;
+}
+
+// bounds[b] = first v with P(v) >= P(n) b / G  (P = exclusive prefix of the vertex costs)
+__global__ void cost_bounds_kernel(const int64_t* __restrict__ P, int64_t n, int G, int32_t* __restrict__ bounds)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > G) return;
+    const double target = (double)P[n] * (double)b / (double)G;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((double)P[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    bounds[b] = b == G ? (int32_t)n : (int32_t)lo;
+}
+
 // per CSR entry: head vertex - first vertex of its piece (CTA ranges `bounds`, pieces of vt)
 __global__ void hoff_kernel(const int64_t* __restrict__ indptr, int64_t n, const int32_t* __restrict__ bounds, int G,
                             int vt, uint16_t* __restrict__ hoff)
@@ -683,8 +713,21 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     A.n_chunks = A.n;
     Scratch bounds, hoff;
     UMAP_TRY(bounds.alloc(sizeof(int32_t) * (size_t)(grid + 1), s));
-    chunk_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(A.indptr, A.n, 1, (int)A.n, grid, bounds.as<int32_t>());
-    UMAP_LAUNCH_CHECK("chunk_bounds_kernel");
+    {
+        static int cdue = -1, cvert = 2;
+        if (cdue < 0) {
+            const char* e = getenv("UMAP_SGD_CDUE");  // tuning knob (cost model of the CTA balance)
+            cdue = e ? atoi(e) : 16;
+        }
+        Scratch cost, pre;
+        UMAP_TRY(cost.alloc(sizeof(int64_t) * (size_t)A.n, s));
+        UMAP_TRY(pre.alloc(sizeof(int64_t) * (size_t)(A.n + 1), s));
+        vertex_cost_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.edges, A.n, cdue, cvert, cost.as<int64_t>());
+        UMAP_LAUNCH_CHECK("vertex_cost_kernel");
+        UMAP_TRY(exclusive_scan<int64_t>(cost.as<int64_t>(), A.n, pre.as<int64_t>(), s));
+        cost_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(pre.as<int64_t>(), A.n, grid, bounds.as<int32_t>());
+        UMAP_LAUNCH_CHECK("cost_bounds_kernel");
+    }
     UMAP_TRY(hoff.alloc(sizeof(uint16_t) * (size_t)std::max<int64_t>(nnz, 1), s));
     hoff_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.n, bounds.as<int32_t>(), grid, A.vt, hoff.as<uint16_t>());
     UMAP_LAUNCH_CHECK("hoff_kernel");
