@@ -1375,6 +1375,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                              (d + 1.0) * u * 2.0 + ((d + 31) / 32 + 5) * u + 3.0 * u;
             ac.margin = (float)(1.1 * c);
         }
+        if (const char* mg = getenv("UMAP_TC_COARSE_MARGIN")) ac.margin = (float)atof(mg);  // measurement only
         UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
         int grp = 1;
         if (const char* g = getenv("UMAP_TC_LIST_GROUP")) grp = std::max(1, atoi(g));  // tuning knob

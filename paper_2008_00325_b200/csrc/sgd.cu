@@ -43,7 +43,7 @@ struct SgdArgs {
     const uint16_t* hoff;    // flat kernel: per CSR entry, head vertex - first vertex of its piece
     int64_t nnz;
     int32_t vt;              // flat kernel: piece size (vertices whose sums are held in shared memory)
-    int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only
+    int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only, 2 = no edge work (flat)
 };
 
 __device__ __forceinline__ float clip4(float v) { return fminf(fmaxf(v, -4.0f), 4.0f); }
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
         float* Yw = par ? A.Y0 : A.Y1;
         const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
         const float ef = (float)epoch, ef1 = (float)(epoch - 1);
-        for (int pv0 = v_lo; pv0 < v_hi; pv0 += vt) {
+        for (int pv0 = v_lo; pv0 < (A.debug & 1 ? v_lo : v_hi); pv0 += vt) {  // debug: profiling only
             const int np = min(vt, v_hi - pv0);
             for (int i = threadIdx.x; i < np; i += blockDim.x) {
 #pragma unroll
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
                 int qa[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) qa[c] = 0;
-                if (act) process_edge<DIM, true, MC>(A, Yr, Yw, epoch, alpha, pv0 + hl, qt[lane], qa);
+                if (act && !(A.debug & 2)) process_edge<DIM, true, MC>(A, Yr, Yw, epoch, alpha, pv0 + hl, qt[lane], qa);
                 long long sv[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) sv[c] = qa[c];
