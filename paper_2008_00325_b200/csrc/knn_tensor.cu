@@ -226,6 +226,9 @@ struct TcArgs {
     const float* thr_d2;    // [n_q][k] exact sorted thresholds
     int k;
     float margin;           // c: |d2~ - d2_exact| < c (|q|^2 + |r|^2)
+    // RANK mode: R2's own rounding relative to d2: R2 lies in
+    // [(d2~ - E) r_lo, (d2~ + E) r_hi]; 1 / 1 when the margin includes it
+    float r_lo, r_hi;
     int32_t* hist;          // [n_q][k] certain bucket counts (written, not accumulated)
     int32_t* amb;           // per (query row, column half) lists of reference rows to re-check
     int amb_cap;            // capacity per list
@@ -457,7 +460,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 float rmax = rn_l;
 #pragma unroll
                 for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-                const float vlim = -0.5f * (tmax + c_m * (qn + rmax));
+                const float vlim = -0.5f * (tmax / a.r_lo + c_m * (qn + rmax));
                 uint32_t cm = 0;  // columns possibly below the largest threshold
 #pragma unroll
                 for (int u = 0; u < 32; ++u) {
@@ -473,7 +476,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     for (int u = 0; u < 32; ++u) {
                         const float rn = __shfl_sync(0xffffffffu, rn_l, u);
                         const float E = c_m * (qn + rn);
-                        const int b_lo = cnt_le16(v[u] - E, thr), b_hi = cnt_le16(v[u] + E, thr);
+                        const int b_lo = cnt_le16((v[u] - E) * a.r_lo, thr), b_hi = cnt_le16((v[u] + E) * a.r_hi, thr);
                         const bool act = (cm >> u) & 1u;
                         if (act && b_hi == b_lo && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
                         if (act && b_hi != b_lo) {
@@ -499,7 +502,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const float d2a = (u & 16) ? w2[1] : w2[0];
                     const float rn = __shfl_sync(0xffffffffu, rn_l, u);
                     const float E = c_m * (qn + rn);
-                    const float hiv = d2a + E, lov = d2a - E;
+                    const float hiv = (d2a + E) * a.r_hi, lov = (d2a - E) * a.r_lo;
                     const int b_hi = cnt_le16(hiv, thr), b_lo = cnt_le16(lov, thr);  // #thresholds <= d2~ +- E
                     const bool amb = has && b_hi != b_lo;
                     if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
@@ -1341,9 +1344,20 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         const double u = std::ldexp(1.0, -24);
         // + the folded norms (BF16-piece representation u S / 2; the adds of the last hi MMA and
         //   the 8 lo-stage MMAs after them onto partial sums up to S: 144 products)
+        // (+ the centring roundings, 4u S)
         const double c = 3.0 * std::ldexp(1.0, -16) * 0.5 + 3.0 * d_pad * 2.0 * u * 0.5 +
-                         ((d + 31) / 32 + 5) * u + (d + 1.0) * u * 2.0 + 2.0 * u + 0.5 * u + 144.0 * 2.0 * u;
+                         ((d + 31) / 32 + 5) * u + 2.0 * u + 0.5 * u + 144.0 * 2.0 * u + 4.0 * u;
         a.margin = (float)(1.1 * c);
+        // R2's own error, relative to d2 itself rather than 2S: |R2 - d2| <= gamma_{d+1} d2, times
+        // 1.1, plus 4u for the fp32 difference and product that apply the factors and the
+        // factors' own rounding
+        const double g = 1.1 * (d + 1.0) * u / (1.0 - (d + 1.0) * u) + 4.0 * u;
+        a.r_lo = (float)(1.0 - g);
+        a.r_hi = (float)(1.0 + g);
+        if (getenv("UMAP_TC_R2_IN_MARGIN")) {  // measurement only: the round-1 form (R2 term in c)
+            a.margin = (float)(1.1 * (c + (d + 1.0) * u * 2.0 - 4.0 * u));
+            a.r_lo = a.r_hi = 1.0f;
+        }
     }
     a.thr_d2 = thr_use; a.k = k;
     if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
