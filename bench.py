@@ -121,7 +121,7 @@ def peaks():
 NCU_NAME = {"knn_tc_kernel (kNN candidates)": "knn_tc_kernel<32, 6, 0",
             "knn_tc_kernel (trust ranks)": "knn_tc_kernel<32, 6, 1",
             "knn_tc_kernel (trust coarse)": "knn_tc_kernel<32, 6, 2",
-            "sgd_persistent_kernel": "sgd_persistent_kernel", "rank_fix_kernel": "rank_fix",
+            "sgd_kernel": "sgd_", "rank_fix_kernel": "rank_fix",
             "rerank_kernel": "rerank_kernel", "thresholds_warp_kernel": "thresholds_warp_kernel",
             "grid_knn_kernel": "grid_knn_kernel", "smooth_knn_kernel": "smooth_knn_kernel"}
 
@@ -158,7 +158,7 @@ def kernel_work(slot, c, st, n_amb, fine_frac=1.0):
         return "tensor", 2.0 * n * n * d * fine_frac, "flop"
     if slot.startswith("knn_tc_kernel"):
         return "tensor", 2.0 * n * n * d, "flop"          # the n x n x d distance contraction, unpadded
-    if slot == "sgd_persistent_kernel":                    # SURVEY 8(d) byte model
+    if slot == "sgd_kernel":                    # SURVEY 8(d) byte model
         return "hbm", 8.0 * st["nnz"] * (N - 1) + 4.0 * dim * (m + 1) * st["positives"] + 8.0 * dim * n * (N - 1), "B"
     # row gathers: mostly served by L2 (Morton / candidate locality), so the HBM fraction is
     # reported separately and may exceed 1 (see `frac_of_hbm`)

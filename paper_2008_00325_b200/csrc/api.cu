@@ -58,7 +58,7 @@ void profile_record(int slot, cudaEvent_t e0, cudaEvent_t e1) { g_prof.push_back
 static const char* const k_prof_names[PROF_NSLOTS] = {
     "knn_tc_kernel (kNN candidates)", "rerank_kernel", "knn_tc_kernel (trust ranks)", "rank_fix_kernel",
     "thresholds_warp_kernel", "grid_knn_kernel", "smooth_knn_kernel", "fuzzy union (5 kernels)",
-    "sgd_persistent_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
+    "sgd_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
     "transform_sgd_kernel", "knn_tc_kernel (trust coarse)", "spectral init (3 kernels x iterations)"};
 void count_launch(int n) { g_launches += n; }
 

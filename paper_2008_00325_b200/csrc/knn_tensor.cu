@@ -1179,17 +1179,22 @@ namespace {
 // more than the L2 sharing of identical lists gains back (the per-block fine pass runs at a 52%
 // L2 hit rate)
 __global__ void compact_flags_kernel(const uint8_t* __restrict__ flags, int64_t nb, int nt, int grp,
-                                     int32_t* __restrict__ list, int32_t* __restrict__ count)
+                                     int32_t* __restrict__ list, int32_t* __restrict__ count, int rot)
 {
+    // rot: block b's list starts at its diagonal tile b nt / nb and wraps around (rows and
+    // columns share the Hilbert order, so concurrently running neighbour blocks start on
+    // neighbouring tiles); 0: ascending
+    const int start = rot ? (int)((int64_t)blockIdx.x * nt / nb) : 0;
     __shared__ int base;
     const int64_t b = blockIdx.x;
     const int64_t g0 = b / grp * grp, g1 = g0 + grp < nb ? g0 + grp : nb;
     if (threadIdx.x == 0) base = 0;
     __syncthreads();
     for (int t0 = 0; t0 < nt; t0 += blockDim.x) {
-        const int t = t0 + threadIdx.x;
+        const int tt = t0 + threadIdx.x;
+        const int t = tt < nt ? (tt + start) % nt : tt;
         bool f = false;
-        if (t < nt)
+        if (tt < nt)
             for (int64_t bb = g0; bb < g1 && !f; ++bb) f = flags[bb * nt + t] != 0;
         const unsigned bal = __ballot_sync(0xffffffffu, f);
         __shared__ int wcnt[32];
@@ -1393,8 +1398,10 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
         int grp = 1;
         if (const char* g = getenv("UMAP_TC_LIST_GROUP")) grp = std::max(1, atoi(g));  // tuning knob
+        int rot = 0;
+        if (const char* r = getenv("UMAP_TC_LIST_ROT")) rot = atoi(r);  // tuning knob
         compact_flags_kernel<<<(unsigned)nqb, 256, 0, s>>>(flags.as<uint8_t>(), nqb, (int)ntl, grp, tl.as<int32_t>(),
-                                                          tcnt.as<int32_t>());
+                                                          tcnt.as<int32_t>(), rot);
         UMAP_LAUNCH_CHECK("compact_flags_kernel");
         a.tile_list = tl.as<int32_t>();
         a.tile_count = tcnt.as<int32_t>();

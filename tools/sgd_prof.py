@@ -8,4 +8,4 @@ for i in range(3):
     U.profile_begin()
     Y, st = U.fit(X, n_neighbors=15, n_epochs=500, knn_mode="tensor")
     p = U.profile_end()
-print(os.environ.get("UMAP_SGD_VARIANT", "0"), "ms_sgd", round(st["ms_sgd"], 2), "kernel", round(p["sgd_persistent_kernel"][0], 2))
+print(os.environ.get("UMAP_SGD_VARIANT", "0"), "ms_sgd", round(st["ms_sgd"], 2), "kernel", round(p["sgd_kernel"][0], 2))
