@@ -1273,7 +1273,7 @@ umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_
 // *overflow != 0 tells the caller to fall back to the exact SIMT kernel.
 umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
                           const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow,
-                          const float* Y, int d_emb, cudaStream_t s)
+                          const float* Y, int d_emb, const int32_t* perm_in, cudaStream_t s)
 {
     *overflow = 0;
     if (rows == 0) return UMAP_OK;
@@ -1286,7 +1286,10 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     if (ordered) {
         UMAP_TRY(perm.alloc(sizeof(int32_t) * (size_t)n, s));
         UMAP_TRY(pos_of.alloc(sizeof(int32_t) * (size_t)n, s));
-        UMAP_TRY(cluster_order(Y, n, d_emb, perm.as<int32_t>(), s));
+        if (perm_in)  // the caller's Hilbert order of Y (trust_penalty computed it for the thresholds)
+            UMAP_CUDA_TRY(cudaMemcpyAsync(perm.p, perm_in, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        else
+            UMAP_TRY(cluster_order(Y, n, d_emb, perm.as<int32_t>(), s));
         order_maps_kernel<<<ceil_div(n, 256), 256, 0, s>>>(perm.as<int32_t>(), n, pos_of.as<int32_t>());
         UMAP_LAUNCH_CHECK("order_maps_kernel");
         UMAP_TRY(keys.alloc(sizeof(uint32_t) * (size_t)rows, s));

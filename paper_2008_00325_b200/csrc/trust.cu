@@ -15,9 +15,10 @@ umap_status rank_count_exact(const float* Xq, int64_t nq, const float* X, int64_
                              int64_t self_offset, const float* thr_d2, const int32_t* thr_id, int32_t* cnt_out,
                              Scratch& tmp, int* n_splits_out, cudaStream_t s);
 
+umap_status cluster_order(const float* Y, int64_t n, int d_emb, int32_t* perm, cudaStream_t s);
 umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, int64_t rows, int k,
                           const float* thr_d2, const int32_t* thr_id, int32_t* hist, int* overflow,
-                          const float* Y, int d_emb, cudaStream_t s);
+                          const float* Y, int d_emb, const int32_t* perm_in, cudaStream_t s);
 
 namespace {
 
@@ -51,13 +52,16 @@ __global__ void thresholds_kernel(const float* __restrict__ X, int d, const int3
 // bulk != 0: rows through the TMA bulk ring (d % 4 == 0, blockDim = 32 RB_WARPS, RB_SMEM smem)
 __global__ void thresholds_warp_kernel(const float* __restrict__ X, int d, const int32_t* __restrict__ emb_idx,
                                        int64_t rows, int64_t row_begin, int k, float* __restrict__ thr_d2,
-                                       int32_t* __restrict__ thr_id, int bulk)
+                                       int32_t* __restrict__ thr_id, int bulk, const int32_t* __restrict__ order)
 {
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     uint32_t bar0 = 0, ph = 0;
     float* ring = bulk ? bulk_ring_setup(bar0) : nullptr;
-    if (r >= rows) return;
+    if (w >= rows) return;
+    // order (optional): rows visited in the Hilbert order of the embedding, so the warps
+    // resident at one time gather neighbour rows of the same 2-D region (L2 reuse)
+    const int64_t r = order ? (int64_t)order[w] : w;
     float key = INFINITY;
     int32_t id = INT32_MAX;
     if (bulk) {
@@ -108,6 +112,13 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
     UMAP_TRY(cnt.alloc(sizeof(int32_t) * (size_t)rows * k, s));
     UMAP_TRY(total.alloc(sizeof(unsigned long long), s));
     UMAP_CUDA_TRY(cudaMemsetAsync(total.p, 0, sizeof(unsigned long long), s));
+    Scratch order;
+    const bool ordered = knn_mode == UMAP_KNN_TENSOR_BF16 && Y && d_emb == 2 && row_begin == 0 && rows == n &&
+                         !getenv("UMAP_TRUST_NO_ORDER");
+    if (ordered) {
+        UMAP_TRY(order.alloc(sizeof(int32_t) * (size_t)n, s));
+        UMAP_TRY(cluster_order(Y, n, d_emb, order.as<int32_t>(), s));
+    }
     if (k <= 32) {
         ProfScope ps(PROF_THRESHOLDS, s);
         // the bulk ring measured slower here (0.79 vs 0.72 ms at C2: k = 15 of 32 lanes busy,
@@ -122,7 +133,8 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
             }
         }
         thresholds_warp_kernel<<<ceil_div(rows * 32, 32 * RB_WARPS), 32 * RB_WARPS, bulk ? RB_SMEM : 0, s>>>(
-            X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(), thr_i.as<int32_t>(), bulk ? 1 : 0);
+            X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(), thr_i.as<int32_t>(), bulk ? 1 : 0,
+            ordered && k <= 32 ? order.as<int32_t>() : nullptr);
         UMAP_LAUNCH_CHECK("thresholds_warp_kernel");
     } else {
         thresholds_kernel<<<ceil_div(rows, 128), 128, 0, s>>>(X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(),
@@ -133,7 +145,7 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
     int overflow = 1;
     if (knn_mode == UMAP_KNN_TENSOR_BF16)
         UMAP_TRY(rank_count_tc(X, n, d, row_begin, rows, k, thr_d.as<float>(), thr_i.as<int32_t>(), cnt.as<int32_t>(),
-                               &overflow, Y, d_emb, s));
+                               &overflow, Y, d_emb, ordered ? order.as<int32_t>() : nullptr, s));
     if (overflow)  // exact mode, or the tensor pass could not certify enough pairs
         UMAP_TRY(rank_count_exact(X + row_begin * (int64_t)d, rows, X, n, d, k, row_begin, thr_d.as<float>(),
                                   thr_i.as<int32_t>(), cnt.as<int32_t>(), tmp, &n_splits, s));
