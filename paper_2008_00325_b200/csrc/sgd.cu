@@ -700,11 +700,14 @@ template <int DIM, int MC>
 umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
 {
     auto kern = sgd_flat_kernel<DIM, MC>;
-    A.vt = std::min(4096, 65536 / (8 * DIM));
+    const int vt_max = std::min(4096, 65536 / (8 * DIM));
+    A.vt = vt_max;
+    if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
     const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
     static bool attr = false;
     if (!attr) {
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const size_t smem_max = sizeof(unsigned long long) * (size_t)DIM * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
         attr = true;
     }
     int per_sm = 0;

@@ -267,6 +267,31 @@ def test_sgd_deterministic_reproducible_and_dims(O):
         assert np.abs(np_(Yg) - ref).max() <= 1e-4
 
 
+def test_sgd_flat_pieces_bitidentical(O, monkeypatch):
+    """The flat deterministic kernel works through each CTA's vertex range in pieces of vt
+    vertices; tiny (and odd) pieces exercise ragged pieces and heads split across steps.  The
+    int64 fixed-point sums make the result independent of the split (R13)."""
+    X, indptr, col, val = _graph(O, n=1500)
+    Y0 = cu(synth.uniform_embedding(1500, 2, seed=4))
+    outs = []
+    for vt in (None, "7", "1"):
+        if vt is None:
+            monkeypatch.delenv("UMAP_SGD_VT", raising=False)
+        else:
+            monkeypatch.setenv("UMAP_SGD_VT", vt)
+        Yg = Y0.clone()
+        U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=1, e_end=40, n_epochs=40, a=A_, b=B_, seed=9)
+        outs.append(np_(Yg))
+    monkeypatch.delenv("UMAP_SGD_VT", raising=False)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    ref = O.optimize(indptr, col, val, np_(Y0), A_, B_, 40, e_begin=1, e_end=2, m=5, seed=9)
+    monkeypatch.setenv("UMAP_SGD_VT", "7")
+    Yg = Y0.clone()
+    U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=1, e_end=2, n_epochs=40, a=A_, b=B_, seed=9)
+    monkeypatch.delenv("UMAP_SGD_VT", raising=False)
+    assert np.abs(np_(Yg) - ref).max() <= 1e-4
+
+
 def test_sgd_positive_count_matches_schedule(O):
     X, indptr, col, val = _graph(O, n=600)
     N = 50
