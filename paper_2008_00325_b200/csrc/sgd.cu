@@ -84,6 +84,30 @@ __device__ __forceinline__ void load_row(const float* Y, int64_t v, float (&y)[D
     }
 }
 
+// L1-cached read (ld.global.ca) for the flat deterministic kernel: within an epoch it only
+// reads the ping-pong buffer Yr (writes go to Yw), and the grid barrier's gpu-scope fence
+// invalidates L1 (CCTL.IVALL) before the next epoch reads what other SMs wrote
+template <int DIM>
+__device__ __forceinline__ void load_row_ca(const float* Y, int64_t v, float (&y)[DIM])
+{
+    if (DIM == 2) {
+        float a, b;
+        asm("ld.global.ca.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "l"(Y + v * 2));
+        y[0] = a; y[1] = b;
+    } else if (DIM == 4) {
+        float a, b, c, d;
+        asm("ld.global.ca.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(Y + v * 4));
+        y[0] = a; y[1] = b; y[2] = c; y[3] = d;
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            float t;
+            asm("ld.global.ca.f32 %0, [%1];" : "=f"(t) : "l"(Y + v * DIM + c));
+            y[c] = t;
+        }
+    }
+}
+
 template <int DIM>
 __device__ __forceinline__ void load_row_ro(const float* Y, int64_t v, float (&y)[DIM])
 {
@@ -110,7 +134,7 @@ __device__ __forceinline__ int qfix(float g) { return __float2int_rn(g * 1677721
 // samples on h.  MC = compile-time M (all negative-sample loads issued before use), or 0
 // for a runtime M.  DET: the head contribution is returned in fixed point (qacc); the
 // tail contribution is the head contribution of (t, h), computed by t's owner.
-template <int DIM, bool DET, int MC>
+template <int DIM, bool DET, int MC, bool L1 = false>
 __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, float* Yw, int epoch, float alpha,
                                              int h, int t, int (&qacc)[DIM])
 {
@@ -131,11 +155,19 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, 
             }
         }
     }
-    load_row<DIM>(Yr, h, yh);
-    load_row<DIM>(Yr, t, yt);
+    if (L1) {
+        load_row_ca<DIM>(Yr, h, yh);
+        load_row_ca<DIM>(Yr, t, yt);
+    } else {
+        load_row<DIM>(Yr, h, yh);
+        load_row<DIM>(Yr, t, yt);
+    }
     if (MC > 0) {
 #pragma unroll
-        for (int p = 0; p < MP; ++p) load_row<DIM>(Yr, vv[p], yv[p]);
+        for (int p = 0; p < MP; ++p) {
+            if (L1) load_row_ca<DIM>(Yr, vv[p], yv[p]);
+            else load_row<DIM>(Yr, vv[p], yv[p]);
+        }
     }
     float s = 0.0f;
 #pragma unroll
@@ -175,7 +207,8 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, 
             if ((p & 3) == 0)
                 rnd = philox4x32_10((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)(p >> 2), A.key0, A.key1);
             v = (int)__umulhi(pick(rnd, p & 3), (uint32_t)A.n);
-            load_row<DIM>(Yr, v, yvv);
+            if (L1) load_row_ca<DIM>(Yr, v, yvv);
+            else load_row<DIM>(Yr, v, yvv);
         }
         if (v == h) continue;
         float s2 = 0.0f;
@@ -401,7 +434,8 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
                 int qa[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) qa[c] = 0;
-                if (act && !(A.debug & 2)) process_edge<DIM, true, MC>(A, Yr, Yw, epoch, alpha, pv0 + hl, qt[lane], qa);
+                if (act && !(A.debug & 2))
+                    process_edge<DIM, true, MC, true>(A, Yr, Yw, epoch, alpha, pv0 + hl, qt[lane], qa);
                 long long sv[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) sv[c] = qa[c];
