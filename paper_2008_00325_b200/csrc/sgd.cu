@@ -734,7 +734,10 @@ template <int DIM, int MC>
 umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
 {
     auto kern = sgd_flat_kernel<DIM, MC>;
-    const int vt_max = std::min(4096, 65536 / (8 * DIM));
+    // pieces of <= 1024 vertices (C2: ~470 per CTA, one piece): the fixed-point sums take
+    // 16 KB of shared memory at DIM 2 and the carveout leaves the rest of the SM's 256 KB to
+    // L1, which caches the gathered positions (ld.global.ca)
+    const int vt_max = std::min(1024, 65536 / (8 * DIM));
     A.vt = vt_max;
     if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
     const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
@@ -742,6 +745,8 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     if (!attr) {
         const size_t smem_max = sizeof(unsigned long long) * (size_t)DIM * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxL1));
         attr = true;
     }
     int per_sm = 0;
