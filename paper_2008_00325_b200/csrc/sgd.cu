@@ -84,6 +84,20 @@ __device__ __forceinline__ void load_row(const float* Y, int64_t v, float (&y)[D
     }
 }
 
+// streamed once per epoch, kept out of L1 (which holds the gathered positions)
+__device__ __forceinline__ int2 ld_stream_i2(const int2* p)
+{
+    int2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int ld_stream_u16(const uint16_t* p)
+{
+    unsigned short r;
+    asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return (int)r;
+}
+
 // L1-cached read (ld.global.ca) for the flat deterministic kernel: within an epoch it only
 // reads the ping-pong buffer Yr (writes go to Yw), and the grid barrier's gpu-scope fence
 // invalidates L1 (CCTL.IVALL) before the next epoch reads what other SMs wrote
@@ -458,14 +472,14 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
             int64_t base = E0 + 32 * warp;
             int2 nrec = make_int2(0, 0);
             int nho = 0;
-            if (base + lane < E1) { nrec = __ldg(A.edges + base + lane); nho = __ldg(A.hoff + base + lane); }
+            if (base + lane < E1) { nrec = ld_stream_i2(A.edges + base + lane); nho = ld_stream_u16(A.hoff + base + lane); }
             for (; base < E1; base += 32 * W) {
                 const int64_t e = base + lane;
                 const int2 rec = nrec;  // records and head offsets prefetched one step ahead
                 const int ho = nho;
                 if (base + 32 * W + lane < E1) {
-                    nrec = __ldg(A.edges + base + 32 * W + lane);
-                    nho = __ldg(A.hoff + base + 32 * W + lane);
+                    nrec = ld_stream_i2(A.edges + base + 32 * W + lane);
+                    nho = ld_stream_u16(A.hoff + base + 32 * W + lane);
                 }
                 const bool due = e < E1 && edge_due_f(__int_as_float(rec.y), ef, ef1);
                 const unsigned ballot = __ballot_sync(0xffffffffu, due);
