@@ -256,7 +256,7 @@ __device__ __forceinline__ void process_edge(const SgdArgs& A, const float* Yr, 
 }
 
 // grid-wide barrier between epochs (cooperative launch guarantees co-residency);
-// the gpu-scope fences order the epoch's writes and invalidate L1.  Monotonic arrival
+// release/acquire at gpu scope order the epoch's writes and invalidate L1.  Monotonic arrival
 // counter: barrier number k (1-based) completes when the counter reaches k * gridDim.x (no
 // reset, one release-add and acquire polling per CTA).  A two-level variant (8 group
 // counters on separate lines) measured no faster at 592 CTAs.
@@ -265,7 +265,9 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int k)
 {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        // the CTA's writes happen-before thread 0's release through the bar.sync above (release
+        // is cumulative), and the acquire poll below invalidates this SM's L1 (CCTL.IVALL)
+        // before the next epoch's L1-cached reads: no separate fence.sc needed
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         const unsigned int target = k * gridDim.x;
         unsigned int v;
