@@ -1334,7 +1334,8 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN / tc_cg()));
     const int64_t qblocks = (rows + TC_BM - 1) / TC_BM;
     constexpr int NL = tc_amb_lists<1>();  // ambiguous-pair lists per row (one per column part)
-    const int cap = 4096 / NL;
+    int cap = 4096 / NL;
+    if (const char* e = getenv("UMAP_TC_AMB_CAP")) cap = std::max(1, atoi(e));  // test knob: force the overflow path
     UMAP_TRY(amb.alloc(sizeof(int32_t) * (size_t)rows * NL * cap, s));
     UMAP_TRY(ambc.alloc(sizeof(int) * (size_t)rows * NL, s));
     const float* thr_use = ordered ? thr_p.as<float>() : thr_d2;

@@ -420,6 +420,22 @@ def test_trust_tensor_exact_penalty(O, n, d, k, kind, emb):
     assert np.array_equal(np_(pen3), pen_ref[17:300]) and S3 == S2
 
 
+def test_trust_tensor_table4_shape_and_overflow_fallback(O, monkeypatch):
+    """Table-4-shaped rows (isotropic blobs, d = 1024): the tensor path's penalty equals the
+    oracle's; with the re-check lists shrunk to 2 pairs per list the tensor pass overflows and
+    the exact SIMT fallback must give the same integer penalty."""
+    n, d, k = 1200, 1024, 15
+    X = synth.iso(n, d, blobs=10, seed=21)
+    Y = synth.uniform_embedding(n, 2, seed=5)
+    S_ref, _ = O.trust_penalty(X, Y, k)
+    T, S = U.trustworthiness(cu(X), cu(Y), k, knn_mode="tensor")
+    assert S == S_ref
+    monkeypatch.setenv("UMAP_TC_AMB_CAP", "2")
+    T2, S2 = U.trustworthiness(cu(X), cu(Y), k, knn_mode="tensor")
+    monkeypatch.delenv("UMAP_TC_AMB_CAP")
+    assert S2 == S_ref and T2 == T
+
+
 def test_trust_identity_is_one():
     X = cu(synth.lowrank(500, 6))
     T, S = U.trustworthiness(X, X, 10)
