@@ -43,6 +43,7 @@ struct SgdArgs {
     const uint16_t* hoff;    // flat kernel: per CSR entry, head vertex - first vertex of its piece
     int64_t nnz;
     int32_t vt;              // flat kernel: piece size (vertices whose sums are held in shared memory)
+    const int2* prec;        // flat kernel, optional: {col | hoff << 21, r} (n < 2^21, vt <= 2048)
     int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only, 2 = no edge work (flat)
 };
 
@@ -474,15 +475,23 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
             int64_t base = E0 + 32 * warp;
             int2 nrec = make_int2(0, 0);
             int nho = 0;
-            if (base + lane < E1) { nrec = ld_stream_i2(A.edges + base + lane); nho = ld_stream_u16(A.hoff + base + lane); }
+            // one 8-byte record per step when the head offset is packed above the column
+            auto ld_rec = [&](int64_t e, int2& r, int& ho) {
+                if (A.prec) {
+                    r = ld_stream_i2(A.prec + e);
+                    ho = (int)((uint32_t)r.x >> 21);
+                    r.x &= 0x1FFFFF;
+                } else {
+                    r = ld_stream_i2(A.edges + e);
+                    ho = ld_stream_u16(A.hoff + e);
+                }
+            };
+            if (base + lane < E1) ld_rec(base + lane, nrec, nho);
             for (; base < E1; base += 32 * W) {
                 const int64_t e = base + lane;
                 const int2 rec = nrec;  // records and head offsets prefetched one step ahead
                 const int ho = nho;
-                if (base + 32 * W + lane < E1) {
-                    nrec = ld_stream_i2(A.edges + base + 32 * W + lane);
-                    nho = ld_stream_u16(A.hoff + base + 32 * W + lane);
-                }
+                if (base + 32 * W + lane < E1) ld_rec(base + 32 * W + lane, nrec, nho);
                 const bool due = e < E1 && edge_due_f(__int_as_float(rec.y), ef, ef1);
                 const unsigned ballot = __ballot_sync(0xffffffffu, due);
                 due_count += __popc(ballot);
@@ -546,6 +555,16 @@ __global__ void cost_bounds_kernel(const int64_t* __restrict__ P, int64_t n, int
         if ((double)P[mid] < target) lo = mid + 1; else hi = mid;
     }
     bounds[b] = b == G ? (int32_t)n : (int32_t)lo;
+}
+
+__global__ void pack_records_kernel(const int2* __restrict__ edges, const uint16_t* __restrict__ hoff, int64_t nnz,
+                                    int2* __restrict__ out)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nnz) {
+        const int2 r = edges[e];
+        out[e] = make_int2((int)((uint32_t)r.x | ((uint32_t)hoff[e] << 21)), r.y);
+    }
 }
 
 // per CSR entry: head vertex - first vertex of its piece (CTA ranges `bounds`, pieces of vt)
@@ -791,6 +810,14 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     UMAP_LAUNCH_CHECK("hoff_kernel");
     A.bounds = bounds.as<int32_t>();
     A.hoff = hoff.as<uint16_t>();
+    Scratch prec;
+    A.prec = nullptr;
+    if (A.n < (1 << 21) && A.vt <= 2048 && nnz > 0 && !getenv("UMAP_SGD_NO_PACK")) {
+        UMAP_TRY(prec.alloc(sizeof(int2) * (size_t)nnz, s));
+        pack_records_kernel<<<ceil_div(nnz, 256), 256, 0, s>>>(A.edges, A.hoff, nnz, prec.as<int2>());
+        UMAP_LAUNCH_CHECK("pack_records_kernel");
+        A.prec = prec.as<int2>();
+    }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(1024), args, smem, s));
