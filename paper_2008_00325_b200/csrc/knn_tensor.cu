@@ -220,6 +220,7 @@ struct TcArgs {
     int exclude_self;
     int64_t index_offset;   // global id = j + index_offset
     int debug;              // bit0: skip epilogue filtering, bit1: skip MMA issue (profiling only)
+    int prefilter;          // MODE 0: skip candidate-free chunks with a max tree first (short K)
     int32_t* cand_idx;      // [split][n_q][kc]
     float* cand_d2;
     // RANK mode (trustworthiness, R16)
@@ -609,6 +610,20 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 // the accumulator holds -d2/2 (norms folded into the GEMM); out-of-range
                 // columns (zero-filled TMA rows) are masked by their index
                 const float nthr = -0.5f * thr;
+                if (a.prefilter) {
+                    // short K (the epilogue bounds the kernel): most chunks hold no candidate for
+                    // any row of the warp; a max tree and one vote skip them before the
+                    // per-column mask is built
+                    float m16[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+                    for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+                        for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
+                    }
+                    if (!__any_sync(0xffffffffu, valid && m16[0] > nthr)) continue;
+                }
                 const int valid_cols = (int)imin64(32, r_hi - jb);
                 uint32_t cm = 0;  // columns of this chunk that beat the running threshold
 #pragma unroll
@@ -1132,6 +1147,8 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     UMAP_TRY(cd.alloc(sizeof(float) * (size_t)n_splits * nq * kc, s));
     TcArgs a{};
     a.qnorm = qnp; a.rnorm = rn.as<float>(); a.nq = nq; a.nr = nr; a.kblocks = d_pad / TC_BK; a.kc = kc;
+    a.prefilter = a.kblocks <= 4 ? 1 : 0;  // K <= 256: the epilogue, not the MMA, bounds the tile
+    if (const char* e = getenv("UMAP_TC_PREFILTER")) a.prefilter = atoi(e);  // tuning knob
     a.split_len = split_len; a.self_shift = self_shift; a.exclude_self = exclude_self;
     a.index_offset = index_offset; a.cand_idx = ci.as<int32_t>(); a.cand_d2 = cd.as<float>();
     {
