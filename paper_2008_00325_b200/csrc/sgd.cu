@@ -769,11 +769,13 @@ template <int DIM, int MC>
 umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
 {
     auto kern = sgd_flat_kernel<DIM, MC>;
-    // pieces of <= 1024 vertices (C2: ~470 per CTA, one piece): the fixed-point sums take
-    // 16 KB of shared memory at DIM 2 and the carveout leaves the rest of the SM's 256 KB to
-    // L1, which caches the gathered positions (ld.global.ca)
-    const int vt_max = std::min(1024, 65536 / (8 * DIM));
-    A.vt = vt_max;
+    // piece size: ~1.25x the mean vertices per CTA, between 1024 and 4096 (C2: ~470 per CTA,
+    // one piece of <= 1024: the fixed-point sums take 16 KB of shared memory at DIM 2 and the
+    // max-L1 carveout leaves the rest of the SM's 256 KB to L1, which caches the gathered
+    // positions; C4, 1M rows: ~6800 per CTA, two pieces of 4096 instead of seven of 1024)
+    const int vt_max = std::min(4096, 65536 / (8 * DIM));
+    const int64_t want_vt = (A.n * 5 / 4) / std::max(1, num_sms()) + 1;
+    A.vt = (int)std::min<int64_t>(vt_max, std::max<int64_t>(std::min(1024, vt_max), want_vt));
     if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
     const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
     static bool attr = false;
