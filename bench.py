@@ -170,13 +170,16 @@ def cfg_of(name):
     return c
 
 
-def kernel_work(slot, c, st, n_amb, fine_frac=1.0):
-    """Algorithmic work of one step of a kernel: (bound, amount, unit)."""
+def kernel_work(slot, c, st, n_amb, fine_frac=1.0, world=1):
+    """Algorithmic work of one step of a kernel on one rank: (bound, amount,
+    unit).  With N ranks the kNN reference rows and the trust rows are sharded (1/N of the
+    contraction and of the thresholds per rank); rerank, graph and SGD run in full on every
+    rank."""
     n, d, k, N, m, dim = c["n"], c["d"], c["k"], c["n_epochs"], 5, 2
     if slot == "knn_tc_kernel (trust ranks)":             # the contraction over the tiles it visits
-        return "tensor", 2.0 * n * n * d * fine_frac, "flop"
+        return "tensor", 2.0 * n * n * d * fine_frac / world, "flop"
     if slot.startswith("knn_tc_kernel"):
-        return "tensor", 2.0 * n * n * d, "flop"          # the n x n x d distance contraction, unpadded
+        return "tensor", 2.0 * n * n * d / world, "flop"  # the n x n x d distance contraction, unpadded
     if slot == "sgd_kernel":                    # SURVEY 8(d) byte model
         return "hbm", 8.0 * st["nnz"] * (N - 1) + 4.0 * dim * (m + 1) * st["positives"] + 8.0 * dim * n * (N - 1), "B"
     # row gathers: mostly served by L2 (Morton / candidate locality), so the HBM fraction is
@@ -186,7 +189,7 @@ def kernel_work(slot, c, st, n_amb, fine_frac=1.0):
     if slot == "rerank_kernel":
         return "gather", 4.0 * d * n * max(32, 2 * k), "B"  # k' candidate rows per query
     if slot == "thresholds_warp_kernel":
-        return "gather", 4.0 * d * n * 15, "B"             # one row per embedding neighbour
+        return "gather", 4.0 * d * n * 15 / world, "B"     # one row per embedding neighbour
     if slot == "smooth_knn_kernel":
         return "hbm", 16.0 * n * k, "B"                    # dist + idx in, w + col out
     return None, None, None
@@ -396,7 +399,7 @@ def run_ours(args):
     kernels = {}
     for name, (tot, cnt) in prof.items():
         per = tot / args.steps
-        bound, work, unit = kernel_work(name, c, st, n_amb, fine_frac)
+        bound, work, unit = kernel_work(name, c, st, n_amb, fine_frac, world)
         rec = {"ms_per_step": per, "launches_per_step": cnt / args.steps, "share_of_step": per / ms}
         if bound == "tensor":
             # burst peak: the measured sustained figure (4 s of back-to-back 8192^3 cuBLAS) sits below
@@ -415,7 +418,7 @@ def run_ours(args):
     roof = None
     if dom:
         r = kernels[dom]
-        bound, work, unit = kernel_work(dom, c, st, n_amb, fine_frac)
+        bound, work, unit = kernel_work(dom, c, st, n_amb, fine_frac, world)
         traffic, tsrc = profile_traffic(dom)
         launches_dom = max(1.0, r["launches_per_step"])
         roof = {"kernel": dom, "bound": r.get("bound"), "achieved": r.get("achieved"), "peak": r.get("peak"),
