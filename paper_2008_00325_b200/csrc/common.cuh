@@ -179,4 +179,11 @@ __device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)
 
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
+// Measurement knobs that make results invalid or uncertified (margin overrides, disabled
+// kernel parts) are read only when UMAP_UNSAFE_EXPERIMENTS is set as well.
+inline const char* unsafe_env(const char* name)
+{
+    return getenv("UMAP_UNSAFE_EXPERIMENTS") ? getenv(name) : nullptr;
+}
+
 }  // namespace umapb200

@@ -1152,7 +1152,7 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     a.split_len = split_len; a.self_shift = self_shift; a.exclude_self = exclude_self;
     a.index_offset = index_offset; a.cand_idx = ci.as<int32_t>(); a.cand_d2 = cd.as<float>();
     {
-        const char* dbg = getenv("UMAP_TC_DEBUG");
+        const char* dbg = unsafe_env("UMAP_TC_DEBUG");
         a.debug = dbg ? atoi(dbg) : 0;
     }
     const dim3 grid((unsigned)qblocks, n_splits);
@@ -1380,15 +1380,15 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         const double g = 1.1 * (d + 1.0) * u / (1.0 - (d + 1.0) * u) + 4.0 * u;
         a.r_lo = (float)(1.0 - g);
         a.r_hi = (float)(1.0 + g);
-        if (getenv("UMAP_TC_R2_IN_MARGIN")) {  // measurement only: the round-1 form (R2 term in c)
+        if (unsafe_env("UMAP_TC_R2_IN_MARGIN")) {  // measurement only: the round-1 form (R2 term in c)
             a.margin = (float)(1.1 * (c + (d + 1.0) * u * 2.0 - 4.0 * u));
             a.r_lo = a.r_hi = 1.0f;
         }
     }
     a.thr_d2 = thr_use; a.k = k;
-    if (const char* mg = getenv("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
+    if (const char* mg = unsafe_env("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
     a.hist = hist_use; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
-    if (const char* dbg = getenv("UMAP_TC_DEBUG")) a.debug = atoi(dbg);  // profiling only (results invalid)
+    if (const char* dbg = unsafe_env("UMAP_TC_DEBUG")) a.debug = atoi(dbg);  // profiling only (results invalid)
     a.dense_min = TC_DENSE_MIN;
     if (const char* dm = getenv("UMAP_TC_DENSE_MIN")) a.dense_min = atoi(dm);  // tuning knob
     a.amb_count = ambc.as<int>();
@@ -1415,7 +1415,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                              (d + 1.0) * u * 2.0 + ((d + 31) / 32 + 5) * u + 3.0 * u;
             ac.margin = (float)(1.1 * c);
         }
-        if (const char* mg = getenv("UMAP_TC_COARSE_MARGIN")) ac.margin = (float)atof(mg);  // measurement only
+        if (const char* mg = unsafe_env("UMAP_TC_COARSE_MARGIN")) ac.margin = (float)atof(mg);  // measurement only
         UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
         int grp = 1;
         if (const char* g = getenv("UMAP_TC_LIST_GROUP")) grp = std::max(1, atoi(g));  // tuning knob

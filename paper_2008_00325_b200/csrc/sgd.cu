@@ -966,7 +966,7 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
     A.bar = bar.as<unsigned int>();
     A.owner = owner.as<uint8_t>();
     {
-        const char* dbg = getenv("UMAP_SGD_DEBUG");
+        const char* dbg = unsafe_env("UMAP_SGD_DEBUG");
         A.debug = dbg ? atoi(dbg) : 0;
     }
     umap_status st;

@@ -1,4 +1,5 @@
 import os, sys
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, "/root/repo")
 import torch, synth
 import paper_2008_00325_b200 as U

@@ -1,5 +1,6 @@
 """SGD launch-shape sweep at C2 (UMAP_SGD_VARIANT read once per process): ms_sgd of 3 fits."""
 import os, sys
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 import paper_2008_00325_b200 as U

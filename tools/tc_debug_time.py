@@ -1,6 +1,7 @@
 """Measurement only: kNN / trust tensor-kernel time with parts disabled (UMAP_TC_DEBUG bit0 =
 no epilogue filtering, bit1 = no MMA issue) to see which part bounds the kernel."""
 import os, sys
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 import paper_2008_00325_b200 as U

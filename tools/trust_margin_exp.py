@@ -1,6 +1,7 @@
 """Measurement only: ambiguous-pair count and trust time of the tensor-mode penalty vs the
 certification margin c (env UMAP_TRUST_MARGIN_EXPERIMENT) at C2 shape."""
 import os, sys, time
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 import paper_2008_00325_b200 as U

@@ -2,6 +2,7 @@
 pairs and rank_fix time at the certified fine margin and at 1e-4 / 7e-5 (what a separate
 lo-product accumulator would allow)."""
 import os, sys
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, os.getcwd())
 import torch, synth
 import paper_2008_00325_b200 as U

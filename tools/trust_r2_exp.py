@@ -1,6 +1,7 @@
 """Measurement: ambiguous pairs, penalty and rank_fix time with R2's error taken relative to d2
 (default) vs folded into the S margin (UMAP_TC_R2_IN_MARGIN, the round-1 form), C2 shape."""
 import os, sys
+os.environ.setdefault("UMAP_UNSAFE_EXPERIMENTS", "1")  # this tool reads measurement-only knobs
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, synth
 import paper_2008_00325_b200 as U
