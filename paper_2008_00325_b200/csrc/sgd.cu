@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(32 * sgd_warps<MINB>(), MINB) sgd_persistent_k
                 int qa[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; ++c) qa[c] = 0;
-                if (act) process_edge<DIM, DET, MC>(A, Yr, Yw, epoch, alpha, v0 + hl, q_t[warp][lane], qa);
+                if (act) process_edge<DIM, DET, MC, true>(A, Yr, Yw, epoch, alpha, v0 + hl, q_t[warp][lane], qa);
                 if (DET) {
                     // queued items are in CSR order, so equal owners are contiguous: segmented
                     // sum over the warp, the last lane of each segment adds it (order-free int sum;
