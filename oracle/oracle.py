@@ -28,6 +28,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "umap_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tools/oracle_mutants.py points this at deliberately broken builds to show the pins catch them
+_LIB_OVERRIDE = os.environ.get("UMAP_ORACLE_LIB")
 
 _c_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _c_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
@@ -38,6 +40,8 @@ _I64, _I32, _F32, _F64, _U64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_float, c
 
 def build(force: bool = False) -> str:
     """Compile the C oracle (gcc -O2 -ffp-contract=off, no fast-math)."""
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
                                "-o", _LIB, _SRC, "-lm"])
