@@ -76,7 +76,10 @@ typedef struct {
     float    min_dist;             /* Eq. 3, default 0.1                           */
     float    spread;               /* default 1.0                                           */
     int32_t  negative_sample_rate; /* m negatives per positive edge, default 5        */
-    float    learning_rate;        /* alpha0, default 1.0 (decays linearly, R10)             */
+    float    learning_rate;        /* alpha0, default 1.0 (decays linearly, R10).  The        */
+                                   /* deterministic mode's int32 fixed-point per-edge sums    */
+                                   /* (R13) need (2 + m) * learning_rate < 32: larger values  */
+                                   /* return INVALID_ARGUMENT in that mode                    */
     float    repulsion_strength;   /* gamma, default 1.0                                    */
     float    a, b;                 /* Phi(d) = 1/(1 + a d^{2b}); 0,0 -> fitted (umap_fit_ab) */
     uint64_t seed;                 /* Philox key for init and negative sampling      */
@@ -128,7 +131,10 @@ UMAP_API umap_status umap_fit(const float* X, int64_t n, int32_t d, const umap_p
 /* f1 pre-computed kNN graph ("accept a k-NN graph that has already been
  * computed", App. A.1): the fit from a3 on.  knn_idx n x k int32 (global ids,
  * self excluded), knn_dist n x k fp32, each row sorted ascending (umap_knn output);
- * k = p->n_neighbors.  Host or device pointers.  Same outputs and errors as umap_fit. */
+ * k = p->n_neighbors.  Host or device pointers.  Same outputs and errors as umap_fit.
+ * The graph is validated on the device before use: every id in [0, n), no row lists
+ * itself or an id twice, every distance finite and >= 0; otherwise INVALID_ARGUMENT
+ * (nothing is read out of bounds).  fit_knn(umap_knn(X)) equals umap_fit(X) bit for bit. */
 UMAP_API umap_status umap_fit_knn(const int32_t* knn_idx, const float* knn_dist, int64_t n, const umap_params* p,
                                   float* Y, umap_fit_stats* stats, void* stream);
 
@@ -247,6 +253,14 @@ UMAP_API umap_status umap_supervised_adjust(const int64_t* indptr, const int32_t
 UMAP_API umap_status umap_trust_penalty(const float* X, int64_t n, int32_t d, const int32_t* emb_idx, int32_t k,
                                int64_t row_begin, int64_t row_end, int32_t knn_mode, const float* Y,
                                int32_t d_emb, int64_t* row_pen, int64_t* penalty, void* stream);
+
+/* R16 normaliser (Alg. 1, garbled return read as Venna & Kaski's):
+ * T = 1 - 2 S / (n k (2n - 3k - 1)) in fp64.  Host only; no CUDA needed.  Returns NaN
+ * unless 1 <= k and 2n - 3k - 1 > 0. */
+UMAP_API double      umap_trust_from_penalty(int64_t penalty, int64_t n, int32_t k);
+/* R15 inference budget: transform_epochs if > 0, else ceil(n_epochs / 3) with n_epochs
+ * defaulted as in umap_params (0 -> 500 if n_train <= 10000 else 200).  Host only. */
+UMAP_API int32_t     umap_transform_epoch_count(int32_t n_epochs, int32_t transform_epochs, int64_t n_train);
 
 UMAP_API const char* umap_status_string(umap_status s);
 UMAP_API const char* umap_last_error(void);

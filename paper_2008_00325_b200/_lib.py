@@ -75,6 +75,8 @@ SIGNATURES = {
                                           P(UmapParams), c_int32, c_int32, c_int32, c_int64, c_int32, c_void_p]),
     "umap_trust_penalty": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_int32, c_int64, c_int64, c_int32,
                                      c_void_p, c_int32, c_void_p, P(c_int64), c_void_p]),
+    "umap_trust_from_penalty": (c_double, [c_int64, c_int64, c_int32]),
+    "umap_transform_epoch_count": (c_int32, [c_int32, c_int32, c_int64]),
     "umap_status_string": (ctypes.c_char_p, [c_int32]),
     "umap_last_error": (ctypes.c_char_p, []),
     "umap_kernel_launch_count": (c_int64, []),

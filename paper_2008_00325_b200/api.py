@@ -4,8 +4,8 @@ of the hot path runs in libumapb200.so; nothing here computes.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
-import math
 
 import torch
 
@@ -18,6 +18,19 @@ KNN_MODES = {"exact": _lib.KNN_EXACT_FP32, "tensor": _lib.KNN_TENSOR_BF16}
 
 def _stream(device=None):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _call(device, name, *args):
+    """Call C entry point `name`(*args, stream) with `device` current and its current stream."""
+    with _on(device):
+        check(getattr(_lib.load(), name)(*args, _stream(device)), name)
+
+
+def _on(device):
+    """Make `device` current for the C call (the library launches on the current device)."""
+    if device is None or (isinstance(device, torch.device) and device.type != "cuda"):
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
 
 
 def _ptr(t):
@@ -81,11 +94,10 @@ def fit(X, out=None, labels=None, **kw):
     st = UmapFitStats()
     dev = X.device if X.is_cuda else out.device if out.is_cuda else None
     if labels is None:
-        check(_lib.load().umap_fit(_ptr(X), n, d, ctypes.byref(p), _ptr(out), ctypes.byref(st), _stream(dev)),
-              "umap_fit")
+        _call(dev, "umap_fit", _ptr(X), n, d, ctypes.byref(p), _ptr(out), ctypes.byref(st))
     else:
-        check(_lib.load().umap_fit_supervised(_ptr(X), n, d, _ptr(labels), ctypes.byref(p), _ptr(out),
-                                              ctypes.byref(st), _stream(dev)), "umap_fit_supervised")
+        _call(dev, "umap_fit_supervised", _ptr(X), n, d, _ptr(labels), ctypes.byref(p), _ptr(out),
+                                              ctypes.byref(st))
     return out, st.as_dict()
 
 
@@ -96,8 +108,7 @@ def spectral_init(indptr, col, val, dim=2, seed=0, iters=300):
     val = _dev(val, torch.float32, "val")
     n = indptr.shape[0] - 1
     Y = torch.empty((n, dim), dtype=torch.float32, device=indptr.device)
-    check(_lib.load().umap_spectral_init(_ptr(indptr), _ptr(col), _ptr(val), n, dim, seed, iters, _ptr(Y),
-                                         _stream(indptr.device)), "umap_spectral_init")
+    _call(indptr.device, "umap_spectral_init", _ptr(indptr), _ptr(col), _ptr(val), n, dim, seed, iters, _ptr(Y))
     return Y
 
 
@@ -113,9 +124,8 @@ def supervised_adjust(indptr, col, val, labels, far_dist=5.0, unknown_dist=1.0):
     oc = torch.empty_like(col)
     ov = torch.empty_like(val)
     nnz = ctypes.c_int64()
-    check(_lib.load().umap_supervised_adjust(_ptr(indptr), _ptr(col), _ptr(val), n, _ptr(labels), far_dist,
-                                             unknown_dist, _ptr(oi), _ptr(oc), _ptr(ov), cap, ctypes.byref(nnz),
-                                             _stream(indptr.device)), "umap_supervised_adjust")
+    _call(indptr.device, "umap_supervised_adjust", _ptr(indptr), _ptr(col), _ptr(val), n, _ptr(labels), far_dist,
+                                             unknown_dist, _ptr(oi), _ptr(oc), _ptr(ov), cap, ctypes.byref(nnz))
     return oi, oc[:nnz.value], ov[:nnz.value]
 
 
@@ -129,8 +139,7 @@ def fit_knn(knn_idx, knn_dist, out=None, **kw):
         out = torch.empty((n, p.n_components), dtype=torch.float32, device=knn_idx.device)
     st = UmapFitStats()
     dev = next((t.device for t in (knn_idx, out) if t.is_cuda), None)
-    check(_lib.load().umap_fit_knn(_ptr(knn_idx), _ptr(knn_dist), n, ctypes.byref(p), _ptr(out), ctypes.byref(st),
-                                   _stream(dev)), "umap_fit_knn")
+    _call(dev, "umap_fit_knn", _ptr(knn_idx), _ptr(knn_dist), n, ctypes.byref(p), _ptr(out), ctypes.byref(st))
     return out, st.as_dict()
 
 
@@ -142,9 +151,8 @@ def transform(X_train, Y_train, Xq, q_offset=0, out=None, **kw):
     if out is None:
         out = torch.empty((Xq.shape[0], p.n_components), dtype=torch.float32, device=Xq.device)
     dev = next((t.device for t in (Xq, X_train, out) if t.is_cuda), None)
-    check(_lib.load().umap_transform(_ptr(X_train), _ptr(Y_train), X_train.shape[0], X_train.shape[1], _ptr(Xq),
-                                     Xq.shape[0], q_offset, ctypes.byref(p), _ptr(out), _stream(dev)),
-          "umap_transform")
+    _call(dev, "umap_transform", _ptr(X_train), _ptr(Y_train), X_train.shape[0], X_train.shape[1], _ptr(Xq),
+                                     Xq.shape[0], q_offset, ctypes.byref(p), _ptr(out))
     return out
 
 
@@ -153,9 +161,8 @@ def trustworthiness(X, Y, k=15, knn_mode="exact"):
     Y = _any(Y, torch.float32, "Y")
     T, S = ctypes.c_double(), ctypes.c_int64()
     dev = next((t.device for t in (X, Y) if t.is_cuda), None)
-    check(_lib.load().umap_trustworthiness(_ptr(X), X.shape[1], _ptr(Y), Y.shape[1], X.shape[0], k,
-                                           KNN_MODES[knn_mode], ctypes.byref(T), ctypes.byref(S), _stream(dev)),
-          "umap_trustworthiness")
+    _call(dev, "umap_trustworthiness", _ptr(X), X.shape[1], _ptr(Y), Y.shape[1], X.shape[0], k,
+                                           KNN_MODES[knn_mode], ctypes.byref(T), ctypes.byref(S))
     return T.value, S.value
 
 
@@ -168,10 +175,10 @@ def knn(Xq, Xr, k, exclude_self=False, query_offset=0, index_offset=0, mode="exa
     nq, d = Xq.shape
     idx = torch.empty((nq, k), dtype=torch.int32, device=Xq.device)
     dist = torch.empty((nq, k), dtype=torch.float32, device=Xq.device)
-    check(_lib.load().umap_knn(_ptr(Xq), nq, _ptr(Xr), Xr.shape[0], d, k, query_offset, index_offset,
+    _call(Xq.device, "umap_knn", _ptr(Xq), nq, _ptr(Xr), Xr.shape[0], d, k, query_offset, index_offset,
                                int(exclude_self), KNN_MODES[mode] if isinstance(mode, str) else mode, int(squared),
                                _ptr(idx),
-                               _ptr(dist), _stream(Xq.device)), "umap_knn")
+                               _ptr(dist))
     return idx, dist
 
 
@@ -182,8 +189,8 @@ def topk_merge(idx_parts, d2_parts, k_out, squared=False):
     n_parts, n, k_in = idx_parts.shape
     idx = torch.empty((n, k_out), dtype=torch.int32, device=idx_parts.device)
     dist = torch.empty((n, k_out), dtype=torch.float32, device=idx_parts.device)
-    check(_lib.load().umap_topk_merge(_ptr(idx_parts), _ptr(d2_parts), n_parts, n, k_in, k_out, int(squared),
-                                      _ptr(idx), _ptr(dist), _stream(idx_parts.device)), "umap_topk_merge")
+    _call(idx_parts.device, "umap_topk_merge", _ptr(idx_parts), _ptr(d2_parts), n_parts, n, k_in, k_out, int(squared),
+                                      _ptr(idx), _ptr(dist))
     return idx, dist
 
 
@@ -198,9 +205,8 @@ def smooth_knn(dist, idx=None, sort_by_col=False):
     if sort_by_col:
         idx = _dev(idx, torch.int32, "idx")
         cs = torch.empty_like(idx)
-    check(_lib.load().umap_smooth_knn(_ptr(dist), _ptr(idx) if idx is not None else ctypes.c_void_p(0), n, k,
-                                      _ptr(rho), _ptr(sigma), _ptr(w), _ptr(cs), _stream(dist.device)),
-          "umap_smooth_knn")
+    _call(dist.device, "umap_smooth_knn", _ptr(dist), _ptr(idx) if idx is not None else ctypes.c_void_p(0), n, k,
+                                      _ptr(rho), _ptr(sigma), _ptr(w), _ptr(cs))
     return (rho, sigma, w, cs) if sort_by_col else (rho, sigma, w)
 
 
@@ -213,14 +219,14 @@ def fuzzy_union(col_sorted_idx, w):
     col = torch.empty(cap, dtype=torch.int32, device=idx.device)
     val = torch.empty(cap, dtype=torch.float32, device=idx.device)
     nnz = ctypes.c_int64()
-    check(_lib.load().umap_fuzzy_union(_ptr(idx), _ptr(w), n, k, _ptr(indptr), _ptr(col), _ptr(val), cap,
-                                       ctypes.byref(nnz), _stream(idx.device)), "umap_fuzzy_union")
+    _call(idx.device, "umap_fuzzy_union", _ptr(idx), _ptr(w), n, k, _ptr(indptr), _ptr(col), _ptr(val), cap,
+                                       ctypes.byref(nnz))
     return indptr, col[:nnz.value], val[:nnz.value]
 
 
 def random_init(n, dim, seed, device="cuda"):
     Y = torch.empty((n, dim), dtype=torch.float32, device=device)
-    check(_lib.load().umap_random_init(n, dim, seed, _ptr(Y), _stream(Y.device)), "umap_random_init")
+    _call(Y.device, "umap_random_init", n, dim, seed, _ptr(Y))
     return Y
 
 
@@ -235,8 +241,8 @@ def optimize(indptr, col, val, Y, e_begin=1, e_end=None, **kw):
     if e_end is None:
         e_end = p.n_epochs
     pos = ctypes.c_int64()
-    check(_lib.load().umap_optimize(_ptr(indptr), _ptr(col), _ptr(val), Y.shape[0], _ptr(Y), ctypes.byref(p),
-                                    e_begin, e_end, ctypes.byref(pos), _stream(Y.device)), "umap_optimize")
+    _call(Y.device, "umap_optimize", _ptr(indptr), _ptr(col), _ptr(val), Y.shape[0], _ptr(Y), ctypes.byref(p),
+                                    e_begin, e_end, ctypes.byref(pos))
     return pos.value
 
 
@@ -249,10 +255,9 @@ def transform_optimize(idx, w, Y_train, Yq, n_epochs_t, e_begin=1, e_end=None, q
     p = params(n_components=Y_train.shape[1], **kw)
     if e_end is None:
         e_end = n_epochs_t
-    check(_lib.load().umap_transform_optimize(_ptr(idx), _ptr(w), idx.shape[0], idx.shape[1], _ptr(Y_train),
+    _call(Yq.device, "umap_transform_optimize", _ptr(idx), _ptr(w), idx.shape[0], idx.shape[1], _ptr(Y_train),
                                               Y_train.shape[0], _ptr(Yq), ctypes.byref(p), n_epochs_t, e_begin,
-                                              e_end, q_offset, int(init), _stream(Yq.device)),
-          "umap_transform_optimize")
+                                              e_end, q_offset, int(init))
     return Yq
 
 
@@ -268,19 +273,21 @@ def trust_penalty(X, emb_idx, k, row_begin=0, row_end=None, knn_mode="exact", Y=
         row_end = n
     pen = torch.empty(row_end - row_begin, dtype=torch.int64, device=X.device)
     S = ctypes.c_int64()
-    check(_lib.load().umap_trust_penalty(_ptr(X), n, X.shape[1], _ptr(emb_idx), k, row_begin, row_end,
+    _call(X.device, "umap_trust_penalty", _ptr(X), n, X.shape[1], _ptr(emb_idx), k, row_begin, row_end,
                                          KNN_MODES[knn_mode], _ptr(Y), Y.shape[1] if Y is not None else 0,
                                          _ptr(pen),
-                                         ctypes.byref(S), _stream(X.device)), "umap_trust_penalty")
+                                         ctypes.byref(S))
     return S.value, pen
 
 
 def trust_from_penalty(S, n, k):
-    return 1.0 - (2.0 / (n * k * (2.0 * n - 3.0 * k - 1.0))) * S
+    """umap_trust_from_penalty (R16 normaliser, computed in the C library)."""
+    return float(_lib.load().umap_trust_from_penalty(int(S), int(n), int(k)))
 
 
-def default_transform_epochs(n_epochs):
-    return int(math.ceil(n_epochs / 3.0))
+def default_transform_epochs(n_epochs, transform_epochs=0, n_train=0):
+    """umap_transform_epoch_count (R15 budget, computed in the C library)."""
+    return int(_lib.load().umap_transform_epoch_count(int(n_epochs), int(transform_epochs), int(n_train)))
 
 
 def kernel_launch_count():

@@ -96,6 +96,49 @@ umap_status any_nonfinite(const float* x, int64_t m, bool* out, cudaStream_t s)
     return UMAP_OK;
 }
 
+// f1 input check (umap_fit_knn): thread per row; flag bit 1 = id out of [0, n) or the row
+// itself, 2 = an id twice in the row, 4 = a distance not finite or negative.  The graph stages
+// index arrays by these ids (indeg/scatter) and assume k distinct neighbours per row.
+__global__ void validate_knn_kernel(const int32_t* __restrict__ idx, const float* __restrict__ dist, int64_t n, int k,
+                                    int* __restrict__ flag)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int32_t* row = idx + i * k;
+    int bad = 0;
+    for (int j = 0; j < k; ++j) {
+        const int32_t c = row[j];
+        if (c < 0 || (int64_t)c >= n || (int64_t)c == i) bad |= 1;
+        for (int l = 0; l < j; ++l) bad |= (row[l] == c) ? 2 : 0;
+        const float dv = dist[i * k + j];
+        if (!isfinite(dv) || dv < 0.0f) bad |= 4;
+    }
+    if (bad) atomicOr(flag, bad);
+}
+
+umap_status validate_knn(const int32_t* idx, const float* dist, int64_t n, int k, cudaStream_t s)
+{
+    Scratch flag;
+    UMAP_TRY(flag.alloc(sizeof(int), s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+    if (n > 0) {
+        validate_knn_kernel<<<ceil_div(n, 128), 128, 0, s>>>(idx, dist, n, k, flag.as<int>());
+        UMAP_LAUNCH_CHECK("validate_knn_kernel");
+    }
+    int h = 0;
+    UMAP_CUDA_TRY(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h) {
+        std::string m = "knn graph rejected:";
+        if (h & 1) m += " id out of [0, n) or equal to its row;";
+        if (h & 2) m += " duplicate id within a row;";
+        if (h & 4) m += " distance not finite or negative;";
+        set_last_error(m);
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    return UMAP_OK;
+}
+
 bool is_device_ptr(const void* p)
 {
     if (!p) return false;
@@ -218,6 +261,17 @@ umap_status check_params(const umap_params* p)
         set_last_error("init must be 0 (random) or 1 (spectral)");
         return UMAP_ERR_INVALID_ARGUMENT;
     }
+    // R13: a due edge's fixed-point contributions (2 q(g_att) + sum of m q(g_rep), each |q| <=
+    // 4 alpha 2^24) are summed in int32 before the segment sums widen to int64
+    if (p->sgd_mode == UMAP_SGD_DETERMINISTIC &&
+        !((2.0 + (double)p->negative_sample_rate) * (double)p->learning_rate < 32.0)) {
+        set_last_error("deterministic SGD needs (2 + negative_sample_rate) * learning_rate < 32 (R13 fixed point)");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
+    if (!(p->learning_rate >= 0.f) || !(p->repulsion_strength >= 0.f)) {
+        set_last_error("learning_rate and repulsion_strength must be finite and >= 0");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
     return UMAP_OK;
 }
 
@@ -254,7 +308,22 @@ using namespace umapb200;
 
 extern "C" {
 
-const char* umap_version(void) { return "umap-b200 0.1 (sm_100a)"; }
+const char* umap_version(void) { return "umap-b200 0.2 (sm_100a)"; }
+
+double umap_trust_from_penalty(int64_t penalty, int64_t n, int32_t k)
+{
+    const double nn = (double)n, kk = (double)k;
+    const double den = nn * kk * (2.0 * nn - 3.0 * kk - 1.0);
+    if (k < 1 || !(den > 0.0)) return std::nan("");
+    return 1.0 - (2.0 / den) * (double)penalty;
+}
+
+int32_t umap_transform_epoch_count(int32_t n_epochs, int32_t transform_epochs, int64_t n_train)
+{
+    if (transform_epochs > 0) return transform_epochs;
+    const int32_t N = n_epochs > 0 ? n_epochs : (n_train <= 10000 ? 500 : 200);
+    return (N + 2) / 3;
+}
 
 int64_t umap_kernel_launch_count(void) { return g_launches; }
 
@@ -763,6 +832,7 @@ umap_status umap_fit_knn(const int32_t* knn_idx, const float* knn_dist, int64_t 
     }
     DevIn dist_d;
     UMAP_TRY(dist_d.make(knn_dist, (size_t)n * k, s));
+    UMAP_TRY(validate_knn(idx_d, dist_d.p, n, k, s));
     DevOut Yd;
     UMAP_TRY(Yd.make(Y, (size_t)n * dim, s));
     umap_fit_stats st{};
@@ -789,7 +859,7 @@ umap_status umap_transform(const float* X_train, const float* Y_train, int64_t n
     if (!X_train || !Y_train || !X_q || !Y_q || d < 1) { set_last_error("null array"); return UMAP_ERR_INVALID_ARGUMENT; }
     if (k < 1 || k > 64 || k > n_train) { set_last_error("1 <= k <= min(64, n_train)"); return UMAP_ERR_K_OUT_OF_RANGE; }
     if (n_q == 0) return UMAP_OK;
-    const int n_t = p.transform_epochs > 0 ? p.transform_epochs : (p.n_epochs + 2) / 3;
+    const int n_t = umap_transform_epoch_count(p.n_epochs, p.transform_epochs, n_train);
     DevIn Xtr, Ytr, Xq;
     UMAP_TRY(Xtr.make(X_train, (size_t)n_train * d, s));
     UMAP_TRY(Ytr.make(Y_train, (size_t)n_train * dim, s));
@@ -849,8 +919,7 @@ umap_status trust_device(const float* Xd, int d, const float* Yd, int d_emb, int
     }
     int64_t S = 0;
     UMAP_TRY(trust_penalty(Xd, n, d, eidx.as<int32_t>(), k, 0, n, nullptr, &S, knn_mode, Yd, d_emb, s));
-    const double nn = (double)n, kk = (double)k;
-    *T = 1.0 - (2.0 / (nn * kk * (2.0 * nn - 3.0 * kk - 1.0))) * (double)S;
+    *T = umap_trust_from_penalty(S, n, k);
     if (penalty) *penalty = S;
     return UMAP_OK;
 }

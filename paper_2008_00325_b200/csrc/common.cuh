@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <string>
 
 #include "../../include/umap_b200.h"
@@ -62,16 +63,35 @@ struct ProfScope {
     }
 };
 
+inline int current_device()
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
+// Function attributes (dynamic shared memory opt-in, carveout) and occupancy are per device:
+// `static PerDeviceOnce once; if (once.first()) {...}` runs the block once on every device a
+// process uses (a process-wide flag skipped it on the second GPU).
+struct PerDeviceOnce {
+    std::atomic<uint64_t> mask{0};
+    bool first()
+    {
+        const uint64_t b = 1ull << (current_device() & 63);
+        return !(mask.fetch_or(b) & b);
+    }
+};
+
 inline int num_sms()
 {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    static int sms[64] = {0};
+    const int dev = current_device() & 63;
+    if (!sms[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device());
+        sms[dev] = v > 0 ? v : 148;
     }
-    return sms;
+    return sms[dev];
 }
 
 // Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync): the RMM-pool

@@ -238,11 +238,10 @@ umap_status smooth_knn(const float* dist, const int32_t* idx, int64_t n, int k, 
     const size_t smem = (size_t)SK_WARPS * 32 * stride * (col_sorted ? 8 : 4) + (col_sorted ? 0 : 0);
     const size_t smem_alloc = (size_t)SK_WARPS * 32 * stride * 8;  // layout assumes both halves
     (void)smem;
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    if (configured.first()) {
         UMAP_CUDA_TRY(cudaFuncSetAttribute(smooth_knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(SK_WARPS * 32 * 65 * 8)));
-        configured = true;
     }
     ProfScope ps(PROF_SMOOTH_KNN, s);
     smooth_knn_kernel<<<ceil_div(n, 32 * SK_WARPS), 32 * SK_WARPS, smem_alloc, s>>>(dist, idx, n, k, rho, sigma,

@@ -209,11 +209,10 @@ template <int KMAX, int MODE>
 umap_status launch_tiles_t(const TileArgs& a, int n_splits, cudaStream_t s)
 {
     const size_t smem = tile_smem_bytes(KMAX, MODE);
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    if (configured.first()) {
         UMAP_CUDA_TRY(cudaFuncSetAttribute(dist_tile_kernel<KMAX, MODE>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
     }
     dim3 grid(ceil_div(a.nq, BM), n_splits);
     ProfScope ps(MODE == 0 ? PROF_KNN_EXACT : PROF_TRUST_EXACT, s);

@@ -1060,11 +1060,10 @@ template <int KC, int ST, int MODE, int CG>
 umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs& a, dim3 grid, cudaStream_t s)
 {
     const size_t smem = knn_tc_smem_bytes<KC, ST, MODE, CG>();
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceOnce configured;
+    if (configured.first()) {
         UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST, MODE, CG>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
     }
     ProfScope ps(MODE == 0 ? PROF_KNN_TC : (MODE == 1 ? PROF_TRUST_TC : PROF_TRUST_COARSE), s);
     if constexpr (CG == 2) {
@@ -1170,10 +1169,9 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     ProfScope ps(PROF_RERANK, s);
     const bool bulk = (d % 4 == 0) && ((uintptr_t)Xq % 16 == 0) && ((uintptr_t)Xr % 16 == 0);
     if (bulk) {
-        static bool cfg = false;
-        if (!cfg) {
+        static PerDeviceOnce cfg;
+        if (cfg.first()) {
             UMAP_CUDA_TRY(cudaFuncSetAttribute(rerank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RB_SMEM));
-            cfg = true;
         }
     }
     rerank_kernel<<<ceil_div(nq * 32, 32 * RB_WARPS), 32 * RB_WARPS, bulk ? RB_SMEM : 0, s>>>(
@@ -1446,11 +1444,10 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         const int32_t* qmap = ordered ? qrow.as<int32_t>() : nullptr;
         const int32_t* cmap = ordered ? perm.as<int32_t>() : nullptr;
         if (d % 4 == 0 && (uintptr_t)X % 16 == 0 && !getenv("UMAP_RANKFIX_LDG")) {  // TMA bulk staging (16-byte aligned rows)
-            static bool cfg = false;
-            if (!cfg) {
+            static PerDeviceOnce cfg;
+            if (cfg.first()) {
                 UMAP_CUDA_TRY(cudaFuncSetAttribute(rank_fix_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)RB_SMEM));
-                cfg = true;
             }
             const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows, RB_WARPS), num_sms());
             rank_fix_bulk_kernel<<<grid, 32 * RB_WARPS, RB_SMEM, s>>>(xq, X, d, rows, amb.as<int32_t>(),

@@ -742,8 +742,9 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
 {
     auto kern = sgd_persistent_kernel<DIM, DET, MC, VPW, MINB, CPB>;
     A.n_chunks = (A.n + VPW - 1) / VPW;
-    static int max_blocks = -1;
-    if (max_blocks < 0) {
+    static int max_blocks_dev[64] = {0};  // per device (occupancy is a per-device property)
+    int& max_blocks = max_blocks_dev[current_device() & 63];
+    if (max_blocks <= 0) {
         int per_sm = 0;
         UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * sgd_warps<MINB>(), 0));
         max_blocks = std::max(1, per_sm) * num_sms();
@@ -778,13 +779,12 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     A.vt = (int)std::min<int64_t>(vt_max, std::max<int64_t>(std::min(1024, vt_max), want_vt));
     if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
     const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    if (attr.first()) {
         const size_t smem_max = sizeof(unsigned long long) * (size_t)DIM * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                            (int)cudaSharedmemCarveoutMaxL1));
-        attr = true;
     }
     int per_sm = 0;
     UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));

@@ -125,11 +125,10 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
         // one batch per row), so the per-lane streaming path is used; the option stays for k > 16
         const bool bulk = k > 16 && (d % 4 == 0) && ((uintptr_t)X % 16 == 0);
         if (bulk) {
-            static bool cfg = false;
-            if (!cfg) {
+            static PerDeviceOnce cfg;
+            if (cfg.first()) {
                 UMAP_CUDA_TRY(cudaFuncSetAttribute(thresholds_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)RB_SMEM));
-                cfg = true;
             }
         }
         thresholds_warp_kernel<<<ceil_div(rows * 32, 32 * RB_WARPS), 32 * RB_WARPS, bulk ? RB_SMEM : 0, s>>>(

@@ -90,8 +90,8 @@ def sharded_trustworthiness(X, Y, k, group=None, knn_fn=None, penalty_fn=None, k
     knn_fn = knn_fn or _default_knn()
     emb_idx, _ = knn_fn(Y, Y, k, exclude_self=True)
     S = sharded_trust_penalty(X, emb_idx, k, group=group, penalty_fn=penalty_fn, knn_mode=knn_mode, Y=Y)
-    n = X.shape[0]
-    return 1.0 - (2.0 / (n * k * (2.0 * n - 3.0 * k - 1.0))) * S, S
+    from . import api
+    return api.trust_from_penalty(S, X.shape[0], k), S
 
 
 def sharded_fit(X, group=None, knn_fn=None, merge_fn=None, fit_knn_fn=None, **kw):
