@@ -117,13 +117,22 @@ def test_fit_c1_all_dims_both_modes_vs_oracle(O, dim):
     Hogwild persistent kernel's gathers are L1-cached since r01): trustworthiness within
     0.005 of the oracle's deterministic fit of the same dimension."""
     X = synth.make("C1")
-    ref = O.fit(X, k=15, n_components=dim, n_epochs=200, a=A_, b=B_, seed=0, mode="deterministic")
-    t_ref = O.trustworthiness(X, ref, 15)
+    # 1-D layouts are chaotic: the GPU's per-epoch agreement (<= 1e-4, teacher-forced,
+    # test_sgd_deterministic_teacher_forced_dims) does not carry a 200-epoch trajectory, and one
+    # seed's trust alone varies by up to 0.017 between seeds on either side (measured,
+    # tools/dim_trust_seeds.py: oracle 0.9589..0.9642, GPU 0.9462..0.9642 over seeds 0-5).  At
+    # DIM 1 the bar is applied to the mean over four seeds (DESIGN.md section 4).
+    seeds = (0, 1, 2, 3) if dim == 1 else (0,)
+    t_ref = np.mean([O.trustworthiness(X, O.fit(X, k=15, n_components=dim, n_epochs=200, a=A_, b=B_, seed=s,
+                                                 mode="deterministic"), 15) for s in seeds])
     for mode in ("deterministic", "hogwild"):
-        Y, _ = U.fit(cu(X), n_neighbors=15, n_components=dim, n_epochs=200, a=A_, b=B_, seed=0, sgd_mode=mode)
-        assert Y.shape == (X.shape[0], dim)
-        T, _ = U.trustworthiness(cu(X), Y, 15)
-        assert abs(T - t_ref) <= 0.005, (dim, mode, T, t_ref)
+        Ts = []
+        for s in seeds:
+            Y, _ = U.fit(cu(X), n_neighbors=15, n_components=dim, n_epochs=200, a=A_, b=B_, seed=s, sgd_mode=mode)
+            assert Y.shape == (X.shape[0], dim)
+            Ts.append(U.trustworthiness(cu(X), Y, 15)[0])
+        T = float(np.mean(Ts))
+        assert abs(T - t_ref) <= 0.005, (dim, mode, Ts, t_ref)
 
 
 @pytest.mark.parametrize("dim", [1, 4, 8])
