@@ -45,7 +45,25 @@ struct SgdArgs {
     int32_t vt;              // flat kernel: piece size (vertices whose sums are held in shared memory)
     const int2* prec;        // flat kernel, optional: {col | hoff << 21, r} (n < 2^21, vt <= 2048)
     int debug;               // profiling knob (UMAP_SGD_DEBUG): 1 = barrier only, 2 = no edge work (flat)
+    // Philox4x32-10 round keys (R11) precomputed on the host: rk0[r] = key0 + r 0x9E3779B9,
+    // rk1[r] = key1 + r 0xBB67AE85.  In the kernel parameter (constant) bank they enter the
+    // round's 3-input XOR as an operand, no per-thread key schedule.
+    uint32_t rk0[10], rk1[10];
+    const int* max_row;      // flat2: device max CSR row length (> 65535: 64-bit CAS accumulation)
 };
+
+__device__ __forceinline__ u32x4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const SgdArgs& A)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned long long p0 = (unsigned long long)0xD2511F53u * c0;
+        const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ A.rk0[r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ A.rk1[r];
+        c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
+    }
+    return {c0, c1, c2, c3};
+}
 
 __device__ __forceinline__ float clip4(float v) { return fminf(fmaxf(v, -4.0f), 4.0f); }
 
@@ -528,15 +546,291 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat_kernel(SgdArgs A)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
 }
 
+// ---------------------------------------------------------------- flat2: lean deterministic SGD
+// The flat kernel's edge work, restructured to issue fewer instructions per due edge (the
+// flat kernel issues ~800 thread-instructions per due edge; ncu r01p):
+//  * Philox round keys from the kernel parameter bank (philox_rk) instead of a per-thread
+//    key schedule;
+//  * the piece's own head rows sit in shared memory (loaded once per piece, also the base of
+//    the final write), only the tail and the m samples are gathered from global memory, all
+//    issued together before any arithmetic (predicated volatile loads: the compiler cannot
+//    sink one into a branch);
+//  * branch-free terms: alpha 2^24 folded into the coefficient (A24 = alpha 2^24 exactly, so
+//    clip4(c d) alpha 2^24 = clamp(c A24 d, +-4 A24) up to the rounding of one product), one
+//    MUFU.RCP per term, the s = 0 and v = head cases by selects (v = head gives d = 0, s = 0
+//    and a zero kick); packed FADD2/FMUL2 at DIM 2;
+//  * fixed-point sums by 32-bit shared reductions of the per-edge sum split at bit 16
+//    (lo = q & 0xFFFF summed unsigned, hi = q >> 16 summed signed; exact while a vertex has
+//    < 65536 due edges per epoch, i.e. every CSR row shorter than 65536 -- else the 64-bit CAS
+//    add), instead of the warp-segmented 64-bit scan.
+// The per-term quantisation q = rint(g 2^24) and the integer sums keep the result independent
+// of the launch shape and of the order of the work (R13).
+template <int DIM>
+__device__ __forceinline__ void gather_row_p(const float* Y, int64_t v, bool p, float (&y)[DIM])
+{
+    const float* a = Y + v * DIM;
+    if (DIM == 2) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q ld.global.ca.v2.f32 {%0, %1}, [%2];\n\t}"
+                     : "+f"(y[0]), "+f"(y[1]) : "l"(a), "r"((int)p));
+    } else if (DIM == 4) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.ca.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+                     : "+f"(y[0]), "+f"(y[1]), "+f"(y[2]), "+f"(y[3]) : "l"(a), "r"((int)p));
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c)
+            asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.ca.f32 %0, [%1];\n\t}"
+                         : "+f"(y[c]) : "l"(a + c), "r"((int)p));
+    }
+}
+
+__device__ __forceinline__ float lg2_ftz(float x)
+{
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_ftz(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+struct TermK {
+    float a, b;     // curve (R8)
+    float katt;     // -2 a b A24
+    float krep;     // 2 gamma b A24
+    float c4;       // 4 A24 (the clip bound in fixed-point units)
+};
+
+// d = yh - yo, s = |d|^2 in the R12 order (s = fmaf(d_c, d_c, s) over c)
+template <int DIM>
+__device__ __forceinline__ float diff_sq(const float (&yh)[DIM], const float (&yo)[DIM], float (&d)[DIM])
+{
+    if (DIM == 2) {
+        unsigned long long H, O, D;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(H) : "f"(yh[0]), "f"(yh[1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(O) : "f"(yo[0]), "f"(yo[1]));
+        asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(D) : "l"(H), "l"(O));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(d[0]), "=f"(d[1]) : "l"(D));
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) d[c] = yh[c] - yo[c];
+    }
+    float s = 0.0f;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) s = fmaf(d[c], d[c], s);
+    return s;
+}
+
+// q_c += sel ? rint(clamp(k d_c, +-c4)) : rint(alt)
+template <int DIM>
+__device__ __forceinline__ void quant_add(float k, const float (&d)[DIM], bool sel, float alt, float c4, int mul,
+                                          int (&q)[DIM])
+{
+    float g[DIM];
+    if (DIM == 2) {
+        unsigned long long D, K, G;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(D) : "f"(d[0]), "f"(d[1]));
+        asm("mov.b64 %0, {%1, %1};" : "=l"(K) : "f"(k));
+        asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(G) : "l"(D), "l"(K));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(g[0]), "=f"(g[1]) : "l"(G));
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) g[c] = k * d[c];
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        const float x = sel ? fminf(fmaxf(g[c], -c4), c4) : alt;
+        q[c] += mul * __float2int_rn(x);
+    }
+}
+
+template <int DIM, int MC>
+__global__ void __launch_bounds__(1024, 1) sgd_flat2_kernel(SgdArgs A)
+{
+    constexpr int W = 32;
+    extern __shared__ __align__(16) unsigned char sgd_smem[];
+    const int vt = A.vt;
+    uint32_t* acc_lo = reinterpret_cast<uint32_t*>(sgd_smem);              // [DIM][vt]
+    int32_t* acc_hi = reinterpret_cast<int32_t*>(acc_lo + (size_t)DIM * vt); // [DIM][vt]
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(sgd_smem);  // wide mode: [DIM][vt]
+    float* yhead = reinterpret_cast<float*>(acc_hi + (size_t)DIM * vt);     // [vt][DIM]
+    int32_t* const qh = reinterpret_cast<int32_t*>(yhead + (size_t)DIM * vt) + (threadIdx.x >> 5) * QCAP;
+    int32_t* const qt = qh + W * QCAP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int v_lo = A.bounds[blockIdx.x], v_hi = A.bounds[blockIdx.x + 1];
+    const bool wide = *A.max_row > 65535;
+    const uint32_t nn = (uint32_t)A.n;
+    unsigned long long due_count = 0;
+    for (int epoch = A.e_begin; epoch < A.e_end; ++epoch) {
+        const int par = (epoch - A.e_begin) & 1;
+        const float* Yr = par ? A.Y1 : A.Y0;
+        float* Yw = par ? A.Y0 : A.Y1;
+        const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
+        const float a24 = __fmul_rn(alpha, 16777216.0f);  // exact (power-of-two scale)
+        TermK K;
+        K.a = A.a; K.b = A.b;
+        K.katt = __fmul_rn(-2.0f * A.a * A.b, a24);
+        K.krep = __fmul_rn(2.0f * A.gamma * A.b, a24);
+        K.c4 = __fmul_rn(4.0f, a24);
+        const float ef = (float)epoch, ef1 = (float)(epoch - 1);
+        for (int pv0 = v_lo; pv0 < v_hi; pv0 += vt) {
+            const int np = min(vt, v_hi - pv0);
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) {
+                    if (wide) acc64[c * vt + i] = 0ull;
+                    else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+                }
+            }
+            for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(Yr + (int64_t)pv0 * DIM + i);
+            __syncthreads();
+            const int64_t E0 = __ldg(A.indptr + pv0), E1 = __ldg(A.indptr + pv0 + np);
+            int qn = 0;
+            auto drain = [&](int count) {
+                const bool act = lane < count;
+                const int hl = act ? qh[lane] : 0;
+                const int t = act ? qt[lane] : pv0;
+                const int h = pv0 + hl;
+                constexpr int MP = MC > 0 ? MC : 1;
+                int vv[MP];
+                float yt[DIM], yv[MP][DIM], yh[DIM];
+                if (MC > 0) {
+#pragma unroll
+                    for (int blk = 0; blk < (MP + 3) / 4; ++blk) {
+                        const u32x4 rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)blk, A);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (4 * blk + i < MP) vv[4 * blk + i] = (int)__umulhi(pick(rnd, i), nn);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) yt[c] = 0.0f;
+                gather_row_p<DIM>(Yr, t, act, yt);
+                if (MC > 0) {
+#pragma unroll
+                    for (int p = 0; p < MP; ++p) {
+#pragma unroll
+                        for (int c = 0; c < DIM; ++c) yv[p][c] = 0.0f;
+                        gather_row_p<DIM>(Yr, vv[p], act, yv[p]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) yh[c] = yhead[hl * DIM + c];
+                int qa[DIM];
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) qa[c] = 0;
+                {   // attractive: head share 2 q(g) (owner computes, R13)
+                    float d[DIM];
+                    const float s = diff_sq<DIM>(yh, yt, d);
+                    const float sb = ex2_approx(K.b * lg2_ftz(s));
+                    const float den = s * fmaf(K.a, sb, 1.0f);
+                    const float k = s > 0.0f ? K.katt * sb * rcp_ftz(den) : 0.0f;
+                    quant_add<DIM>(k, d, true, 0.0f, K.c4, 2, qa);
+                }
+                const int pend = MC > 0 ? MC : A.m;
+                u32x4 rnd = {0, 0, 0, 0};
+#pragma unroll
+                for (int p = 0; p < pend; ++p) {
+                    int v;
+                    float yvv[DIM];
+                    if (MC > 0) {
+                        v = vv[MC > 0 ? p : 0];
+#pragma unroll
+                        for (int c = 0; c < DIM; ++c) yvv[c] = yv[MC > 0 ? p : 0][c];
+                    } else {
+                        if ((p & 3) == 0) rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)(p >> 2), A);
+                        v = (int)__umulhi(pick(rnd, p & 3), nn);
+#pragma unroll
+                        for (int c = 0; c < DIM; ++c) yvv[c] = 0.0f;
+                        gather_row_p<DIM>(Yr, v, act, yvv);
+                    }
+                    float d[DIM];
+                    const float s2 = diff_sq<DIM>(yh, yvv, d);
+                    const float sb = ex2_approx(K.b * lg2_ftz(s2));
+                    const float k = K.krep * rcp_ftz((0.001f + s2) * fmaf(K.a, sb, 1.0f));
+                    // s2 = 0: +4 alpha per component unless v is the head itself (then d = 0, no term)
+                    quant_add<DIM>(k, d, s2 > 0.0f, v != h ? K.c4 : 0.0f, K.c4, 1, qa);
+                }
+                if (act) {
+#pragma unroll
+                    for (int c = 0; c < DIM; ++c) {
+                        if (!wide) {
+                            atomicAdd(acc_lo + c * vt + hl, (uint32_t)qa[c] & 0xFFFFu);
+                            atomicAdd(acc_hi + c * vt + hl, qa[c] >> 16);
+                        } else {
+                            atomicAdd(acc64 + c * vt + hl, (unsigned long long)(long long)qa[c]);
+                        }
+                    }
+                }
+            };
+            int64_t base = E0 + 32 * warp;
+            int2 nrec = make_int2(0, 0);
+            int nho = 0;
+            auto ld_rec = [&](int64_t e, int2& r, int& ho) {
+                if (A.prec) {
+                    r = ld_stream_i2(A.prec + e);
+                    ho = (int)((uint32_t)r.x >> 21);
+                    r.x &= 0x1FFFFF;
+                } else {
+                    r = ld_stream_i2(A.edges + e);
+                    ho = ld_stream_u16(A.hoff + e);
+                }
+            };
+            if (base + lane < E1) ld_rec(base + lane, nrec, nho);
+            for (; base < E1; base += 32 * W) {
+                const int64_t e = base + lane;
+                const int2 rec = nrec;
+                const int ho = nho;
+                if (base + 32 * W + lane < E1) ld_rec(base + 32 * W + lane, nrec, nho);
+                const bool due = e < E1 && edge_due_f(__int_as_float(rec.y), ef, ef1);
+                const unsigned ballot = __ballot_sync(0xffffffffu, due);
+                due_count += __popc(ballot);
+                if (due) {
+                    const int pos = qn + __popc(ballot & ((1u << lane) - 1u));
+                    qh[pos] = ho;
+                    qt[pos] = rec.x;
+                }
+                __syncwarp();
+                qn += __popc(ballot);
+                if (qn >= 32) {
+                    drain(32);
+                    qn -= 32;
+                    __syncwarp();
+                    if (lane < qn) { qh[lane] = qh[32 + lane]; qt[lane] = qt[32 + lane]; }
+                    __syncwarp();
+                }
+            }
+            if (qn > 0) drain(qn);
+            __syncthreads();
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int v = pv0 + i;
+#pragma unroll
+                for (int c = 0; c < DIM; ++c) {
+                    const long long tot = wide ? (long long)acc64[c * vt + i]
+                                               : (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
+                    Yw[(int64_t)v * DIM + c] = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
+                }
+            }
+            __syncthreads();
+        }
+        if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1));
+    }
+    if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
 // Expected per-epoch cost of vertex v's work in the flat kernel, in units of 1/256 record
 // scan: every record is scanned each epoch, record e is due in a fraction ~r_e of the epochs
 // (R9) and then costs cdue scans' worth (the gathers and the gradient), plus cvert for the
 // vertex's own read-modify-write.
 __global__ void vertex_cost_kernel(const int64_t* __restrict__ indptr, const int2* __restrict__ edges, int64_t n,
-                                   int cdue, int cvert, int64_t* __restrict__ cost)
+                                   int cdue, int cvert, int64_t* __restrict__ cost, int* __restrict__ max_row)
 {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
+    const int64_t len = indptr[v + 1] - indptr[v];
+    atomicMax(max_row, len > INT32_MAX ? INT32_MAX : (int)len);
     int64_t c = 256LL * cvert;
     for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e)
         c += 256 + (int64_t)(256.0f * (float)cdue * __int_as_float(edges[e].y));
@@ -767,9 +1061,9 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
 }
 
 template <int DIM, int MC>
-umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
+umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, bool v2)
 {
-    auto kern = sgd_flat_kernel<DIM, MC>;
+    auto kern = v2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
     // piece size: ~1.25x the mean vertices per CTA, between 1024 and 4096 (C2: ~470 per CTA,
     // one piece of <= 1024: the fixed-point sums take 16 KB of shared memory at DIM 2 and the
     // max-L1 carveout leaves the rest of the SM's 256 KB to L1, which caches the gathered
@@ -778,10 +1072,12 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     const int64_t want_vt = (A.n * 5 / 4) / std::max(1, num_sms()) + 1;
     A.vt = (int)std::min<int64_t>(vt_max, std::max<int64_t>(std::min(1024, vt_max), want_vt));
     if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
-    const size_t smem = sizeof(unsigned long long) * (size_t)DIM * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
-    static PerDeviceOnce attr;
-    if (attr.first()) {
-        const size_t smem_max = sizeof(unsigned long long) * (size_t)DIM * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
+    // flat2 adds the piece's head rows (4 DIM B per vertex) to the fixed-point sums (8 DIM B)
+    const size_t per_v = (sizeof(unsigned long long) + (v2 ? sizeof(float) : 0)) * (size_t)DIM;
+    const size_t smem = per_v * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
+    static PerDeviceOnce attr[2];
+    if (attr[v2].first()) {
+        const size_t smem_max = per_v * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                            (int)cudaSharedmemCarveoutMaxL1));
@@ -801,7 +1097,9 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
         Scratch cost, pre;
         UMAP_TRY(cost.alloc(sizeof(int64_t) * (size_t)A.n, s));
         UMAP_TRY(pre.alloc(sizeof(int64_t) * (size_t)(A.n + 1), s));
-        vertex_cost_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.edges, A.n, cdue, cvert, cost.as<int64_t>());
+        UMAP_CUDA_TRY(cudaMemsetAsync(const_cast<int*>(A.max_row), 0, sizeof(int), s));
+        vertex_cost_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.edges, A.n, cdue, cvert, cost.as<int64_t>(),
+                                                              const_cast<int*>(A.max_row));
         UMAP_LAUNCH_CHECK("vertex_cost_kernel");
         UMAP_TRY(exclusive_scan<int64_t>(cost.as<int64_t>(), A.n, pre.as<int64_t>(), s));
         cost_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(pre.as<int64_t>(), A.n, grid, bounds.as<int32_t>());
@@ -823,7 +1121,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s)
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(1024), args, smem, s));
-    UMAP_LAUNCH_CHECK("sgd_flat_kernel");
+    UMAP_LAUNCH_CHECK(v2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
     return UMAP_OK;
 }
 
@@ -868,8 +1166,9 @@ umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
 template <int DIM>
 umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
 {
-    if (DIM <= 4 && det && sgd_variant() == 0) {  // DIM 8, 16: 64 registers per thread spill
-        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s) : launch_sgd_flat<DIM, 0>(A, A.nnz, s);
+    if (DIM <= 4 && det && (sgd_variant() == 0 || sgd_variant() == 100)) {  // DIM 8, 16: 64 registers per thread spill
+        const bool v2 = sgd_variant() == 0;  // 100: the round-1 flat kernel (A/B comparisons)
+        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, v2) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, v2);
     }
     if (A.m == 5) return det ? launch_sgd_m<DIM, true, 5>(A, s) : launch_sgd_m<DIM, false, 5>(A, s);
     return det ? launch_sgd_m<DIM, true, 0>(A, s) : launch_sgd_m<DIM, false, 0>(A, s);
@@ -962,6 +1261,13 @@ umap_status optimize_layout(const int64_t* indptr, const int32_t* col, const flo
     A.a = p->a; A.b = p->b; A.gamma = p->repulsion_strength; A.alpha0 = p->learning_rate;
     A.n_epochs = p->n_epochs; A.e_begin = e_begin; A.e_end = e_end; A.m = p->negative_sample_rate;
     A.key0 = (uint32_t)p->seed; A.key1 = (uint32_t)(p->seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        A.rk0[r] = A.key0 + (uint32_t)r * 0x9E3779B9u;
+        A.rk1[r] = A.key1 + (uint32_t)r * 0xBB67AE85u;
+    }
+    Scratch maxrow;
+    UMAP_TRY(maxrow.alloc(sizeof(int), s));
+    A.max_row = maxrow.as<int>();
     A.positives = counter.as<unsigned long long>();
     A.bar = bar.as<unsigned int>();
     A.owner = owner.as<uint8_t>();
