@@ -49,7 +49,9 @@ struct SgdArgs {
     // rk1[r] = key1 + r 0xBB67AE85.  In the kernel parameter (constant) bank they enter the
     // round's 3-input XOR as an operand, no per-thread key schedule.
     uint32_t rk0[10], rk1[10];
-    const int* max_row;      // flat2: device max CSR row length (> 65535: 64-bit CAS accumulation)
+    const int* max_row;      // flat2/3: device max CSR row length (> 65535: 64-bit CAS accumulation)
+    int list_cap;            // flat3: due-list capacity (>= every CTA's record count)
+    int scan_split_pct;      // flat3: % of the next epoch's scan done before the grid barrier's arrive
 };
 
 __device__ __forceinline__ u32x4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const SgdArgs& A)
@@ -646,6 +648,105 @@ __device__ __forceinline__ void quant_add(float k, const float (&d)[DIM], bool s
     }
 }
 
+// Edge work of one due edge (h = v0 + hl, t) at epoch `epoch` for the lean kernels: the head's
+// fixed-point contribution qa (2 q(g_att) + sum of the m repulsive q(g), R12/R13).  yhead holds
+// the head rows of the vertices [v0, ...).  act = false: the gathers are predicated off and qa is
+// meaningless (the caller does not add it).
+template <int DIM, int MC>
+__device__ __forceinline__ void edge_terms(const SgdArgs& A, const float* Yr, int epoch, uint32_t nn, const TermK& K,
+                                           const float* yhead, int v0, int hl, int t, bool act, int (&qa)[DIM])
+{
+    const int h = v0 + hl;
+    constexpr int MP = MC > 0 ? MC : 1;
+    int vv[MP];
+    float yt[DIM], yv[MP][DIM], yh[DIM];
+    if (MC > 0) {
+#pragma unroll
+        for (int blk = 0; blk < (MP + 3) / 4; ++blk) {
+            const u32x4 rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)blk, A);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (4 * blk + i < MP) vv[4 * blk + i] = (int)__umulhi(pick(rnd, i), nn);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) yt[c] = 0.0f;
+    gather_row_p<DIM>(Yr, t, act, yt);
+    if (MC > 0) {
+#pragma unroll
+        for (int p = 0; p < MP; ++p) {
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) yv[p][c] = 0.0f;
+            gather_row_p<DIM>(Yr, vv[p], act, yv[p]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) yh[c] = yhead[hl * DIM + c];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) qa[c] = 0;
+    {   // attractive: head share 2 q(g) (owner computes, R13)
+        float d[DIM];
+        const float s = diff_sq<DIM>(yh, yt, d);
+        const float sb = ex2_approx(K.b * lg2_ftz(s));
+        const float den = s * fmaf(K.a, sb, 1.0f);
+        const float k = s > 0.0f ? K.katt * sb * rcp_ftz(den) : 0.0f;
+        quant_add<DIM>(k, d, true, 0.0f, K.c4, 2, qa);
+    }
+    const int pend = MC > 0 ? MC : A.m;
+    u32x4 rnd = {0, 0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < pend; ++p) {
+        int v;
+        float yvv[DIM];
+        if (MC > 0) {
+            v = vv[MC > 0 ? p : 0];
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) yvv[c] = yv[MC > 0 ? p : 0][c];
+        } else {
+            if ((p & 3) == 0) rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)(p >> 2), A);
+            v = (int)__umulhi(pick(rnd, p & 3), nn);
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) yvv[c] = 0.0f;
+            gather_row_p<DIM>(Yr, v, act, yvv);
+        }
+        float d[DIM];
+        const float s2 = diff_sq<DIM>(yh, yvv, d);
+        const float sb = ex2_approx(K.b * lg2_ftz(s2));
+        const float k = K.krep * rcp_ftz((0.001f + s2) * fmaf(K.a, sb, 1.0f));
+        // s2 = 0: +4 alpha per component unless v is the head itself (then d = 0, no term)
+        quant_add<DIM>(k, d, s2 > 0.0f, v != h ? K.c4 : 0.0f, K.c4, 1, qa);
+    }
+}
+
+// add a per-edge fixed-point sum to the head's accumulators (16-bit split, or 64-bit CAS when
+// some CSR row has >= 65536 entries)
+template <int DIM>
+__device__ __forceinline__ void acc_add(uint32_t* acc_lo, int32_t* acc_hi, unsigned long long* acc64, int stride,
+                                        int hl, bool wide, const int (&qa)[DIM])
+{
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        if (!wide) {
+            atomicAdd(acc_lo + c * stride + hl, (uint32_t)qa[c] & 0xFFFFu);
+            atomicAdd(acc_hi + c * stride + hl, qa[c] >> 16);
+        } else {
+            atomicAdd(acc64 + c * stride + hl, (unsigned long long)(long long)qa[c]);
+        }
+    }
+}
+
+__device__ __forceinline__ TermK epoch_terms(const SgdArgs& A, int epoch)
+{
+    const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
+    const float a24 = __fmul_rn(alpha, 16777216.0f);  // exact (power-of-two scale)
+    TermK K;
+    K.a = A.a; K.b = A.b;
+    K.katt = __fmul_rn(-2.0f * A.a * A.b, a24);
+    K.krep = __fmul_rn(2.0f * A.gamma * A.b, a24);
+    K.c4 = __fmul_rn(4.0f, a24);
+    return K;
+}
+
 template <int DIM, int MC>
 __global__ void __launch_bounds__(1024, 1) sgd_flat2_kernel(SgdArgs A)
 {
@@ -667,13 +768,7 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat2_kernel(SgdArgs A)
         const int par = (epoch - A.e_begin) & 1;
         const float* Yr = par ? A.Y1 : A.Y0;
         float* Yw = par ? A.Y0 : A.Y1;
-        const float alpha = __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs)));
-        const float a24 = __fmul_rn(alpha, 16777216.0f);  // exact (power-of-two scale)
-        TermK K;
-        K.a = A.a; K.b = A.b;
-        K.katt = __fmul_rn(-2.0f * A.a * A.b, a24);
-        K.krep = __fmul_rn(2.0f * A.gamma * A.b, a24);
-        K.c4 = __fmul_rn(4.0f, a24);
+        const TermK K = epoch_terms(A, epoch);
         const float ef = (float)epoch, ef1 = (float)(epoch - 1);
         for (int pv0 = v_lo; pv0 < v_hi; pv0 += vt) {
             const int np = min(vt, v_hi - pv0);
@@ -692,78 +787,9 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat2_kernel(SgdArgs A)
                 const bool act = lane < count;
                 const int hl = act ? qh[lane] : 0;
                 const int t = act ? qt[lane] : pv0;
-                const int h = pv0 + hl;
-                constexpr int MP = MC > 0 ? MC : 1;
-                int vv[MP];
-                float yt[DIM], yv[MP][DIM], yh[DIM];
-                if (MC > 0) {
-#pragma unroll
-                    for (int blk = 0; blk < (MP + 3) / 4; ++blk) {
-                        const u32x4 rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)blk, A);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if (4 * blk + i < MP) vv[4 * blk + i] = (int)__umulhi(pick(rnd, i), nn);
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < DIM; ++c) yt[c] = 0.0f;
-                gather_row_p<DIM>(Yr, t, act, yt);
-                if (MC > 0) {
-#pragma unroll
-                    for (int p = 0; p < MP; ++p) {
-#pragma unroll
-                        for (int c = 0; c < DIM; ++c) yv[p][c] = 0.0f;
-                        gather_row_p<DIM>(Yr, vv[p], act, yv[p]);
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < DIM; ++c) yh[c] = yhead[hl * DIM + c];
                 int qa[DIM];
-#pragma unroll
-                for (int c = 0; c < DIM; ++c) qa[c] = 0;
-                {   // attractive: head share 2 q(g) (owner computes, R13)
-                    float d[DIM];
-                    const float s = diff_sq<DIM>(yh, yt, d);
-                    const float sb = ex2_approx(K.b * lg2_ftz(s));
-                    const float den = s * fmaf(K.a, sb, 1.0f);
-                    const float k = s > 0.0f ? K.katt * sb * rcp_ftz(den) : 0.0f;
-                    quant_add<DIM>(k, d, true, 0.0f, K.c4, 2, qa);
-                }
-                const int pend = MC > 0 ? MC : A.m;
-                u32x4 rnd = {0, 0, 0, 0};
-#pragma unroll
-                for (int p = 0; p < pend; ++p) {
-                    int v;
-                    float yvv[DIM];
-                    if (MC > 0) {
-                        v = vv[MC > 0 ? p : 0];
-#pragma unroll
-                        for (int c = 0; c < DIM; ++c) yvv[c] = yv[MC > 0 ? p : 0][c];
-                    } else {
-                        if ((p & 3) == 0) rnd = philox_rk((uint32_t)h, (uint32_t)t, (uint32_t)epoch, (uint32_t)(p >> 2), A);
-                        v = (int)__umulhi(pick(rnd, p & 3), nn);
-#pragma unroll
-                        for (int c = 0; c < DIM; ++c) yvv[c] = 0.0f;
-                        gather_row_p<DIM>(Yr, v, act, yvv);
-                    }
-                    float d[DIM];
-                    const float s2 = diff_sq<DIM>(yh, yvv, d);
-                    const float sb = ex2_approx(K.b * lg2_ftz(s2));
-                    const float k = K.krep * rcp_ftz((0.001f + s2) * fmaf(K.a, sb, 1.0f));
-                    // s2 = 0: +4 alpha per component unless v is the head itself (then d = 0, no term)
-                    quant_add<DIM>(k, d, s2 > 0.0f, v != h ? K.c4 : 0.0f, K.c4, 1, qa);
-                }
-                if (act) {
-#pragma unroll
-                    for (int c = 0; c < DIM; ++c) {
-                        if (!wide) {
-                            atomicAdd(acc_lo + c * vt + hl, (uint32_t)qa[c] & 0xFFFFu);
-                            atomicAdd(acc_hi + c * vt + hl, qa[c] >> 16);
-                        } else {
-                            atomicAdd(acc64 + c * vt + hl, (unsigned long long)(long long)qa[c]);
-                        }
-                    }
-                }
+                edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, pv0, hl, t, act, qa);
+                if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
             };
             int64_t base = E0 + 32 * warp;
             int2 nrec = make_int2(0, 0);
@@ -816,6 +842,181 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat2_kernel(SgdArgs A)
             __syncthreads();
         }
         if (epoch + 1 < A.e_end) grid_barrier(A.bar, (unsigned int)(epoch - A.e_begin + 1));
+    }
+    if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
+// ---------------------------------------------------------------- flat3: one piece per CTA
+// When every CTA's vertex range fits one piece (<= 2048 vertices; n < 2^21 so that a due edge
+// packs into 32 bits as hl << 21 | t, the packed record's own layout) the epoch is split into
+// two phases that overlap across the epoch boundary:
+//   A(e)  scan: warps claim 32-record steps from a shared counter, evaluate the closed-form
+//         schedule (R9) and append the due edges to the CTA's due list for epoch e;
+//   B(e)  edge work: warps claim 32-edge batches of that list from a shared counter.
+// Only the CTA's last batch of an epoch is partial (the flat kernels leave one partial batch
+// per warp per piece), the batches balance the warps dynamically, and a warp that finds no
+// batch left goes on with A(e+1) into the other list (the scan does not read positions), so
+// the tail of B(e) is filled with the next epoch's scan.  The piece's head rows stay in shared
+// memory across epochs: the CTA computes Y_{e+1} of its own vertices itself.  Lists hold up to
+// the CTA's record count (every record due), so they never overflow.
+template <int DIM, int MC>
+__global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
+{
+    extern __shared__ __align__(16) unsigned char sgd_smem[];
+    const int vt = A.vt;        // >= the largest CTA range
+    const int cap = A.list_cap;  // >= the largest CTA record count
+    uint32_t* acc_lo = reinterpret_cast<uint32_t*>(sgd_smem);                  // [DIM][vt]
+    int32_t* acc_hi = reinterpret_cast<int32_t*>(acc_lo + (size_t)DIM * vt);     // [DIM][vt]
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(sgd_smem);  // wide mode: [DIM][vt]
+    float* yhead = reinterpret_cast<float*>(acc_hi + (size_t)DIM * vt);         // [vt][DIM]
+    uint32_t* list0 = reinterpret_cast<uint32_t*>(yhead + (size_t)DIM * vt);    // [2][cap]
+    __shared__ int s_step, s_batch, s_cur[2], s_nlist;
+    const int lane = threadIdx.x & 31;
+    const int v_lo = A.bounds[blockIdx.x], v_hi = A.bounds[blockIdx.x + 1];
+    const int np = v_hi - v_lo;
+    const bool wide = *A.max_row > 65535;
+    const uint32_t nn = (uint32_t)A.n;
+    const int64_t E0 = __ldg(A.indptr + v_lo), E1 = __ldg(A.indptr + v_hi);
+    const int n_steps = (int)((E1 - E0 + 31) >> 5);
+    unsigned long long due_count = 0;
+
+    // A(e): claim groups of SG 32-record steps until `limit` steps are taken; due edges go to list
+    // `buf`.  The next group is claimed before the current one is processed and all SG record
+    // loads of a group are issued together (the claim and load latencies overlap the work).
+    constexpr int SG = 4;
+    auto scan = [&](int e, int buf, int limit) {
+        const float ef = (float)e, ef1 = (float)(e - 1);
+        uint32_t* list = list0 + (size_t)buf * cap;
+        int g = 0;
+        if (lane == 0) g = atomicAdd(&s_step, SG);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        while (g < limit) {
+            int gn = 0;
+            if (lane == 0) gn = atomicAdd(&s_step, SG);
+            int2 rec[SG];
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int64_t ei = E0 + 32 * (int64_t)(g + k) + lane;
+                rec[k] = make_int2(0, 0);
+                if (g + k < limit && ei < E1) {
+                    if (A.prec) {
+                        rec[k] = ld_stream_i2(A.prec + ei);
+                    } else {
+                        rec[k] = ld_stream_i2(A.edges + ei);
+                        rec[k].x |= ld_stream_u16(A.hoff + ei) << 21;
+                    }
+                }
+            }
+            unsigned ballot[SG];
+            int tot = 0;
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int64_t ei = E0 + 32 * (int64_t)(g + k) + lane;
+                const bool due = g + k < limit && ei < E1 && edge_due_f(__int_as_float(rec[k].y), ef, ef1);
+                ballot[k] = __ballot_sync(0xffffffffu, due);
+                tot += __popc(ballot[k]);
+            }
+            due_count += tot;
+            int base = 0;
+            if (lane == 0 && tot) base = atomicAdd(&s_cur[buf], tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                if ((ballot[k] >> lane) & 1u) list[base + __popc(ballot[k] & ((1u << lane) - 1u))] = (uint32_t)rec[k].x;
+                base += __popc(ballot[k]);
+            }
+            g = __shfl_sync(0xffffffffu, gn, 0);
+        }
+    };
+    // the scan of epoch e + 1 is split: steps [0, split) fill the tail of B(e), steps
+    // [split, n_steps) overlap the grid barrier
+    int split = n_steps;
+    {
+        const int pct = A.scan_split_pct;
+        split = (int)(((int64_t)n_steps * pct / 100 + SG - 1) / SG * SG);
+        if (split > n_steps) split = n_steps;
+    }
+
+    for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(A.Y0 + (int64_t)v_lo * DIM + i);
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            if (wide) acc64[c * vt + i] = 0ull;
+            else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+        }
+    }
+    if (threadIdx.x == 0) { s_step = 0; s_batch = 0; s_cur[0] = 0; s_cur[1] = 0; }
+    __syncthreads();
+    scan(A.e_begin, A.e_begin & 1, n_steps);
+    __syncthreads();
+    if (threadIdx.x == 0) { s_nlist = s_cur[A.e_begin & 1]; s_step = 0; }
+    __syncthreads();
+
+    for (int epoch = A.e_begin; epoch < A.e_end; ++epoch) {
+        const int par = (epoch - A.e_begin) & 1;
+        const float* Yr = par ? A.Y1 : A.Y0;
+        float* Yw = par ? A.Y0 : A.Y1;
+        const TermK K = epoch_terms(A, epoch);
+        const int buf = epoch & 1;
+        const uint32_t* list = list0 + (size_t)buf * cap;
+        const int nl = s_nlist;
+        const int nb = (nl + 31) >> 5;
+        // B(epoch): the next batch is claimed before the current one is processed
+        int b = 0;
+        if (lane == 0) b = atomicAdd(&s_batch, 1);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        while (b < nb) {
+            int bn = 0;
+            if (lane == 0) bn = atomicAdd(&s_batch, 1);
+            const int j = 32 * b + lane;
+            const bool act = j < nl;
+            const uint32_t ent = act ? list[j] : 0u;
+            const int hl = (int)(ent >> 21), t = act ? (int)(ent & 0x1FFFFFu) : v_lo;
+            int qa[DIM];
+            edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, hl, t, act, qa);
+            if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
+            b = __shfl_sync(0xffffffffu, bn, 0);
+        }
+        // A(epoch + 1), first part: fills the tail of B(epoch)
+        if (epoch + 1 < A.e_end) scan(epoch + 1, buf ^ 1, split);
+        __syncthreads();
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            const int v = v_lo + i;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                long long tot;
+                if (wide) { tot = (long long)acc64[c * vt + i]; acc64[c * vt + i] = 0ull; }
+                else {
+                    tot = (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
+                    acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0;
+                }
+                const float y = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
+                yhead[i * DIM + c] = y;
+                Yw[(int64_t)v * DIM + c] = y;
+            }
+        }
+        if (epoch + 1 < A.e_end) {
+            // split grid barrier: arrive, finish the scan of epoch + 1, then wait
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+                s_step = split;
+            }
+            __syncthreads();
+            scan(epoch + 1, buf ^ 1, n_steps);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_nlist = s_cur[buf ^ 1]; s_cur[buf] = 0; s_batch = 0; s_step = 0;
+                const unsigned int target = (unsigned int)(epoch - A.e_begin + 1) * gridDim.x;
+                unsigned int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.bar) : "memory");
+                } while (v < target);
+            }
+            __syncthreads();
+        } else {
+            __syncthreads();
+        }
     }
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
 }
@@ -1060,31 +1261,24 @@ umap_status launch_sgd_t(SgdArgs A, cudaStream_t s)
     return UMAP_OK;
 }
 
-template <int DIM, int MC>
-umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, bool v2)
+// largest CTA vertex range and record count of the flat split (flat3 sizing)
+__global__ void cta_extent_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ bounds, int G,
+                                  int* __restrict__ out)
 {
-    auto kern = v2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
-    // piece size: ~1.25x the mean vertices per CTA, between 1024 and 4096 (C2: ~470 per CTA,
-    // one piece of <= 1024: the fixed-point sums take 16 KB of shared memory at DIM 2 and the
-    // max-L1 carveout leaves the rest of the SM's 256 KB to L1, which caches the gathered
-    // positions; C4, 1M rows: ~6800 per CTA, two pieces of 4096 instead of seven of 1024)
-    const int vt_max = std::min(4096, 65536 / (8 * DIM));
-    const int64_t want_vt = (A.n * 5 / 4) / std::max(1, num_sms()) + 1;
-    A.vt = (int)std::min<int64_t>(vt_max, std::max<int64_t>(std::min(1024, vt_max), want_vt));
-    if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
-    // flat2 adds the piece's head rows (4 DIM B per vertex) to the fixed-point sums (8 DIM B)
-    const size_t per_v = (sizeof(unsigned long long) + (v2 ? sizeof(float) : 0)) * (size_t)DIM;
-    const size_t smem = per_v * A.vt + 2 * sizeof(int32_t) * 32 * QCAP;
-    static PerDeviceOnce attr[2];
-    if (attr[v2].first()) {
-        const size_t smem_max = per_v * vt_max + 2 * sizeof(int32_t) * 32 * QCAP;
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                           (int)cudaSharedmemCarveoutMaxL1));
-    }
-    int per_sm = 0;
-    UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
-    const int grid = std::max(1, std::min(per_sm, 1) * num_sms());
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= G) return;
+    const int lo = bounds[b], hi = bounds[b + 1];
+    atomicMax(out, hi - lo);
+    const int64_t rec = indptr[hi] - indptr[lo];
+    atomicMax(out + 1, rec > INT32_MAX ? INT32_MAX : (int)rec);
+}
+
+// ver: 1 = the round-1 flat kernel, 2 = flat2, 3 = flat3 when every CTA range fits one piece
+// (else flat2)
+template <int DIM, int MC>
+umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
+{
+    const int grid = num_sms();  // one CTA of 32 warps per SM (checked against the occupancy below)
     A.n_chunks = A.n;
     Scratch bounds, hoff;
     UMAP_TRY(bounds.alloc(sizeof(int32_t) * (size_t)(grid + 1), s));
@@ -1105,6 +1299,57 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, bool v2)
         cost_bounds_kernel<<<ceil_div(grid + 1, 256), 256, 0, s>>>(pre.as<int64_t>(), A.n, grid, bounds.as<int32_t>());
         UMAP_LAUNCH_CHECK("cost_bounds_kernel");
     }
+    constexpr size_t QBYTES = 2 * sizeof(int32_t) * 32 * QCAP;
+    const int vt_max = std::min(4096, 65536 / (8 * DIM));
+    size_t smem = 0;
+    if (ver == 3 && A.n < (1 << 21) && !getenv("UMAP_SGD_VT")) {
+        Scratch ext;
+        UMAP_TRY(ext.alloc(2 * sizeof(int), s));
+        UMAP_CUDA_TRY(cudaMemsetAsync(ext.p, 0, 2 * sizeof(int), s));
+        cta_extent_kernel<<<ceil_div(grid, 256), 256, 0, s>>>(A.indptr, bounds.as<int32_t>(), grid, ext.as<int>());
+        UMAP_LAUNCH_CHECK("cta_extent_kernel");
+        int h[2] = {0, 0};
+        UMAP_CUDA_TRY(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        const int vt3 = std::max(32, (h[0] + 31) & ~31);
+        const int cap = std::max(32, (h[1] + 31) & ~31);
+        smem = (size_t)(sizeof(unsigned long long) + sizeof(float)) * DIM * vt3 + 2 * sizeof(uint32_t) * (size_t)cap;
+        if (vt3 <= 2048 && smem <= 200 * 1024) {
+            A.vt = vt3;
+            A.list_cap = cap;
+            const char* e = getenv("UMAP_SGD_SCAN_SPLIT");  // tuning knob (% of the scan before the barrier)
+            A.scan_split_pct = e ? std::max(0, std::min(100, atoi(e))) : 50;
+        } else {
+            ver = 2;
+        }
+    } else if (ver == 3) {
+        ver = 2;
+    }
+    if (ver != 3) {
+        // piece size: ~1.25x the mean vertices per CTA, between 1024 and 4096 (C2: ~470 per CTA,
+        // one piece of <= 1024: the fixed-point sums take 16 KB of shared memory at DIM 2 and the
+        // max-L1 carveout leaves the rest of the SM's 256 KB to L1, which caches the gathered
+        // positions; C4, 1M rows: ~6800 per CTA, two pieces of 4096 instead of seven of 1024)
+        const int64_t want_vt = (A.n * 5 / 4) / std::max(1, num_sms()) + 1;
+        A.vt = (int)std::min<int64_t>(vt_max, std::max<int64_t>(std::min(1024, vt_max), want_vt));
+        if (const char* e = getenv("UMAP_SGD_VT")) A.vt = std::max(1, std::min(vt_max, atoi(e)));  // test knob: piece size
+        // flat2 adds the piece's head rows (4 DIM B per vertex) to the fixed-point sums (8 DIM B)
+        const size_t per_v = (sizeof(unsigned long long) + (ver == 2 ? sizeof(float) : 0)) * (size_t)DIM;
+        smem = per_v * A.vt + QBYTES;
+    }
+    auto kern = ver == 3 ? sgd_flat3_kernel<DIM, MC> : ver == 2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
+    static PerDeviceOnce attr[4];
+    if (attr[ver].first()) {
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           (int)cudaSharedmemCarveoutMaxL1));
+    }
+    int per_sm = 0;
+    UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
+    if (per_sm < 1) {
+        set_last_error("SGD kernel does not fit one CTA per SM");
+        return UMAP_ERR_CUDA;
+    }
     UMAP_TRY(hoff.alloc(sizeof(uint16_t) * (size_t)std::max<int64_t>(nnz, 1), s));
     hoff_kernel<<<ceil_div(A.n, 256), 256, 0, s>>>(A.indptr, A.n, bounds.as<int32_t>(), grid, A.vt, hoff.as<uint16_t>());
     UMAP_LAUNCH_CHECK("hoff_kernel");
@@ -1121,7 +1366,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, bool v2)
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(1024), args, smem, s));
-    UMAP_LAUNCH_CHECK(v2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
+    UMAP_LAUNCH_CHECK(ver == 3 ? "sgd_flat3_kernel" : ver == 2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
     return UMAP_OK;
 }
 
@@ -1166,9 +1411,11 @@ umap_status launch_sgd_m(const SgdArgs& A, cudaStream_t s)
 template <int DIM>
 umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
 {
-    if (DIM <= 4 && det && (sgd_variant() == 0 || sgd_variant() == 100)) {  // DIM 8, 16: 64 registers per thread spill
-        const bool v2 = sgd_variant() == 0;  // 100: the round-1 flat kernel (A/B comparisons)
-        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, v2) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, v2);
+    const int sv = sgd_variant();
+    if (DIM <= 4 && det && (sv == 0 || sv == 100 || sv == 101)) {  // DIM 8, 16: 64 registers per thread spill
+        // 100: the round-1 flat kernel, 101: flat2 (A/B comparisons); default flat3 (else flat2)
+        const int ver = sv == 100 ? 1 : sv == 101 ? 2 : 3;
+        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver);
     }
     if (A.m == 5) return det ? launch_sgd_m<DIM, true, 5>(A, s) : launch_sgd_m<DIM, false, 5>(A, s);
     return det ? launch_sgd_m<DIM, true, 0>(A, s) : launch_sgd_m<DIM, false, 0>(A, s);

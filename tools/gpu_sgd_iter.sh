@@ -7,9 +7,9 @@ timeout 900 python -m pytest tests -m gpu -q -x -k "$K" 2>&1 | tail -5 > gpurun_
 for vt in 0 256 700; do
   if [ $vt = 0 ]; then timeout 300 python tools/sgd_same.py; else UMAP_SGD_VT=$vt timeout 300 python tools/sgd_same.py; fi
 done > gpurun_out/sgd_same_${TAG}.log 2>&1
-UMAP_SGD_VARIANT=100 timeout 300 python tools/sgd_same.py >> gpurun_out/sgd_same_${TAG}.log 2>&1
+UMAP_SGD_VARIANT=101 timeout 300 python tools/sgd_same.py >> gpurun_out/sgd_same_${TAG}.log 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
-UMAP_SGD_VARIANT=100 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${TAG}_old.json 2>> gpurun_out/bench_${TAG}.err
+UMAP_SGD_VARIANT=101 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${TAG}_old.json 2>> gpurun_out/bench_${TAG}.err
 cat gpurun_out/pytest_sgd_${TAG}.log gpurun_out/sgd_same_${TAG}.log
 for f in gpurun_out/bench_${TAG}.json gpurun_out/bench_${TAG}_old.json; do
 python - "$f" <<'PY'
