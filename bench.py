@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--sgd-mode", default="deterministic", choices=["deterministic", "hogwild"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-scaling-legs", action="store_true",
+                    help="skip the C4 sharded-kNN and C5 distributed-inference legs")
     return ap.parse_args()
 
 
@@ -196,45 +198,53 @@ def kernel_work(slot, c, st, n_amb, fine_frac=1.0, world=1):
 
 
 # ----------------------------------------------------------------------------- cpu oracle timing
-def oracle_step_estimate(X, k, n_epochs, knn_rows=32, graph_rows=2000, sgd_epochs=6, trust_rows=32, trust_k=15):
-    """Time the CPU oracle (1 thread, as it stands) on bounded samples of one step and
-    extrapolate to the full step: kNN and trust rows are independent (linear in rows);
-    the graph stages and SGD are timed on a `graph_rows` sub-problem and scaled by
-    n / graph_rows (nnz per row is constant) and by the epoch count."""
+def oracle_step_estimate(X, k, n_epochs, knn_rows=32, graph_rows=2000, sgd_epochs=6, trust_rows=32, trust_k=15,
+                         threads=None):
+    """Time the CPU oracle (as it stands) on bounded samples of one step and extrapolate to the
+    full step: kNN and trust rows are independent (linear in rows; the oracle splits them over
+    `threads` OpenMP threads, default all cores); the graph stages and SGD are timed on a
+    `graph_rows` sub-problem and scaled by n / graph_rows (nnz per row is constant) and by the
+    epoch count (the SGD is single-threaded by definition, R13/R14)."""
     import numpy as np
     from oracle import oracle as O
     O.build()
-    n = X.shape[0]
-    rng = np.random.default_rng(0)
-    rows = np.sort(rng.choice(n, knn_rows, replace=False))
-    t0 = time.perf_counter()
-    for r in rows:
-        O.knn(X[r:r + 1], X, k, self_offset=int(r))
-    t_knn = (time.perf_counter() - t0) * n / knn_rows
-    Xs = X[:graph_rows]
-    idx, dist = O.knn(Xs, Xs, k, self_offset=0)  # untimed: input of the graph stages
-    t0 = time.perf_counter()
-    rho, sigma = O.smooth_knn(dist)
-    w = O.membership(dist, rho, sigma)
-    indptr, col, val = O.fuzzy_union(idx, w)
-    t_graph = (time.perf_counter() - t0) * n / graph_rows
-    Y0 = O.random_init(graph_rows, 2, 0)
-    a, b = 1.5769434603, 0.8950608779
-    t0 = time.perf_counter()
-    O.optimize(indptr, col, val, Y0, a, b, n_epochs, e_begin=1, e_end=1 + sgd_epochs, m=5, seed=0)
-    t_sgd = (time.perf_counter() - t0) * (n / graph_rows) * (n_epochs - 1) / sgd_epochs
-    Y = O.random_init(n, 2, 1)
-    trows = np.sort(rng.choice(n, trust_rows, replace=False))
-    t0 = time.perf_counter()
-    for r in trows:
-        O.trust_penalty(X, Y, trust_k, int(r), int(r) + 1)
-    t_trust = (time.perf_counter() - t0) * n / trust_rows
+    all_threads = O.get_threads()
+    if threads:
+        O.set_threads(threads)
+    used = O.get_threads()
+    try:
+        n = X.shape[0]
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(n, knn_rows, replace=False))
+        Xq = np.ascontiguousarray(X[rows])
+        t0 = time.perf_counter()
+        O.knn(Xq, X, k)  # the self row is the first neighbour here: the same work as excluding it
+        t_knn = (time.perf_counter() - t0) * n / knn_rows
+        Xs = X[:graph_rows]
+        idx, dist = O.knn(Xs, Xs, k, self_offset=0)  # untimed: input of the graph stages
+        t0 = time.perf_counter()
+        rho, sigma = O.smooth_knn(dist)
+        w = O.membership(dist, rho, sigma)
+        indptr, col, val = O.fuzzy_union(idx, w)
+        t_graph = (time.perf_counter() - t0) * n / graph_rows
+        Y0 = O.random_init(graph_rows, 2, 0)
+        a, b = 1.5769434603, 0.8950608779
+        t0 = time.perf_counter()
+        O.optimize(indptr, col, val, Y0, a, b, n_epochs, e_begin=1, e_end=1 + sgd_epochs, m=5, seed=0)
+        t_sgd = (time.perf_counter() - t0) * (n / graph_rows) * (n_epochs - 1) / sgd_epochs
+        Y = O.random_init(n, 2, 1)
+        r0 = int(rng.integers(0, n - trust_rows))
+        t0 = time.perf_counter()
+        O.trust_penalty(X, Y, trust_k, r0, r0 + trust_rows)
+        t_trust = (time.perf_counter() - t0) * n / trust_rows
+    finally:
+        O.set_threads(all_threads)
     total = t_knn + t_graph + t_sgd + t_trust
-    sample = (f"oracle 1 thread: kNN {knn_rows} query rows x {n} refs (x{n / knn_rows:.0f}); graph+union on "
-              f"{graph_rows} rows (x{n / graph_rows:.0f}); SGD {sgd_epochs} epochs on that graph "
-              f"(x{(n / graph_rows) * (n_epochs - 1) / sgd_epochs:.0f}); trust {trust_rows} rows x {n} (x{n / trust_rows:.0f}); "
-              f"extrapolated linearly to one full step")
-    return total, {"knn_s": t_knn, "graph_s": t_graph, "sgd_s": t_sgd, "trust_s": t_trust}, sample
+    sample = (f"oracle, {used} thread(s): kNN {knn_rows} query rows x {n} refs (x{n / knn_rows:.0f}); graph+union "
+              f"on {graph_rows} rows (x{n / graph_rows:.0f}); SGD (1 thread) {sgd_epochs} epochs on that graph "
+              f"(x{(n / graph_rows) * (n_epochs - 1) / sgd_epochs:.0f}); trust {trust_rows} rows x {n} "
+              f"(x{n / trust_rows:.0f}); extrapolated linearly to one full step")
+    return total, {"knn_s": t_knn, "graph_s": t_graph, "sgd_s": t_sgd, "trust_s": t_trust}, sample, used
 
 
 def run_reference(args):
@@ -247,9 +257,10 @@ def run_reference(args):
     X = synth.lowrank(c["n"], c["d"], c["blobs"], c["seed"])
     times = []
     parts = None
+    cores = os.cpu_count() or 1
     for i in range(args.warmup + args.steps):
-        t, parts, sample = oracle_step_estimate(X, c["k"], c["n_epochs"], knn_rows=8, graph_rows=1000, sgd_epochs=3,
-                                                trust_rows=8)
+        t, parts, sample, used = oracle_step_estimate(X, c["k"], c["n_epochs"], knn_rows=8 * cores, graph_rows=1000,
+                                                      sgd_epochs=3, trust_rows=8 * cores)
         if i >= args.warmup:
             times.append(t)
     v = sum(times) / len(times)
@@ -259,7 +270,7 @@ def run_reference(args):
             "config": {"workload": f"{args.config} lowrank {c['n']}x{c['d']} k={c['k']} 2-D {c['n_epochs']} epochs"
                                    f" fit + trust(k=15)", "l2": "n/a (CPU)"},
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample,
+            "cpu_baseline": {"value": v, "unit": "s", "cores": used, "kind": "oracle", "sample": sample,
                              "stages_s": parts},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -384,6 +395,7 @@ def run_ours(args):
                "timer": "host wall clock around the synchronous call, after one untimed call",
                "calls_ms": [round(x, 2) for x in e2e_ms]}
     clk = clocks.stop()
+    legs = None if args.no_scaling_legs else scaling_legs(args, world, rank)
 
     if rank != 0:
         if world > 1:
@@ -464,16 +476,156 @@ def run_ours(args):
         "e2e": e2e,
         "peaks": {"source": pk_kind, "hbm_gbs": pk.get("hbm_gbs"), "bf16_tflops": pk.get("bf16_tflops"),
                   "bf16_tflops_sustained": pk.get("bf16_tflops_sustained")},
+        "scaling_legs": legs,
     }
     if not args.no_cpu_baseline and world == 1:
-        t_cpu, parts, sample = oracle_step_estimate(np.ascontiguousarray(X_host.numpy()), k, N, knn_rows=96,
-                                                    graph_rows=2000, sgd_epochs=30, trust_rows=96)
-        line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": 1, "kind": "oracle", "sample": sample,
-                                "stages_s": parts, "host_cpu": _cpu_model()}
+        Xn = np.ascontiguousarray(X_host.numpy())
+        cores = os.cpu_count() or 1
+        # all host cores (the oracle's row loops under OpenMP), then one thread on a smaller sample
+        t_cpu, parts, sample, used = oracle_step_estimate(Xn, k, N, knn_rows=24 * cores, graph_rows=3000,
+                                                          sgd_epochs=40, trust_rows=24 * cores)
+        t_1, parts_1, sample_1, _ = oracle_step_estimate(Xn, k, N, knn_rows=48, graph_rows=2000, sgd_epochs=20,
+                                                         trust_rows=48, threads=1)
+        line["cpu_baseline"] = {"value": t_cpu, "unit": "s", "cores": used, "kind": "oracle", "sample": sample,
+                                "stages_s": parts, "host_cpu": _cpu_model(),
+                                "one_thread": {"value": t_1, "cores": 1, "sample": sample_1, "stages_s": parts_1}}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- scaling legs
+def scaling_legs(args, world, rank, warmup=1, steps=2):
+    """The two BASELINE.json configs that the paper scales across GPUs (App. B P:343,
+    P:480-485), timed at every N (weak in the index rows per rank for C4, partitioned for C5):
+
+    * C4: kNN of 1,000,000 x 50 rows, the reference rows sharded over the ranks, per-rank search
+      of all queries + NCCL all-gather of the n x k (id, d2) candidates + merge (dist.sharded_knn);
+    * C5: the model fitted on 100,000 x 784 rows (untimed, rank 0) is broadcast, every rank embeds
+      its 8,000,000 / N rows (1M-row chunks drawn on the device, global query ids) and the
+      partitions are all-gathered (dist.distributed_inference).
+
+    Each step is bracketed by a barrier + synchronize, timed with CUDA events on the current
+    stream, max over ranks.  `sha1` hashes the merged kNN / the gathered embedding: equal hashes
+    across N show the sharded results are bit-identical to N = 1."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2008_00325_b200 as U
+    from paper_2008_00325_b200 import dist as D
+
+    A_, B_ = 1.5769434603, 0.8950608779
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxr(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sha(*ts):
+        h = hashlib.sha1()
+        for t in ts:
+            h.update(t.contiguous().cpu().numpy().tobytes())
+        return h.hexdigest()[:16]
+
+    out = {}
+    # ---- C4 sharded kNN
+    c = synth.CONFIGS["C4"]
+    X4 = torch.from_numpy(synth.lowrank(c["n"], c["d"], c["blobs"], c["seed"])).cuda()
+    k = c["k"]
+
+    def knn_fn(Xq, Xr, kk, **a):
+        return U.knn(Xq, Xr, kk, mode=args.knn_mode, **a)
+
+    ms, ms_search, ms_gather = [], [], []
+    res = None
+    for i in range(warmup + steps):
+        marks = {}
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+
+        def mark(name):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks[name] = ev
+        barrier()
+        e0.record()
+        res = D.sharded_knn(X4, k, knn_fn=knn_fn, phase_mark=mark)
+        e1.record()
+        barrier()
+        if i >= warmup:
+            ms.append(e0.elapsed_time(e1))
+            ms_search.append(e0.elapsed_time(marks["searched"]))
+            ms_gather.append(marks["searched"].elapsed_time(marks["gathered"]))
+    t4 = maxr(sum(ms) / len(ms))
+    c4 = {"workload": f"C4 lowrank {c['n']}x{c['d']} k={k}, kNN ({args.knn_mode} mode) with the reference rows "
+                      f"sharded x{world}, NCCL all-gather + merge", "n_gpus": world, "ms": t4,
+          "search_ms_max": maxr(sum(ms_search) / len(ms_search)),
+          "allgather_ms_max": maxr(sum(ms_gather) / len(ms_gather)),
+          "allgather_bytes_per_rank": int(world * c["n"] * k * 8) if world > 1 else 0,
+          "queries_per_s": c["n"] / (t4 / 1e3), "sha1": sha(*res), "steps": steps, "warmup": warmup}
+    if world > 1 and rank == 0:  # untimed: the single-GPU result on rank 0, compared row by row
+        si, sd = U.knn(X4, X4, k, exclude_self=True, mode=args.knn_mode)
+        same = ((si == res[0]).all(1) & (sd == res[1]).all(1))
+        c4["rows_identical_to_single_gpu"] = int(same.sum().item())
+        c4["single_gpu_sha1"] = sha(si, sd)
+        del si, sd
+    out["C4_sharded_knn"] = c4
+    del X4, res
+    torch.cuda.empty_cache()
+
+    # ---- C5 distributed inference
+    n_tr, n_q, chunk = 100000, 8000000, 1000000
+    model = synth.lowrank_model(784, 10, 4)
+    if rank == 0:
+        Xtr = torch.from_numpy(synth.lowrank_sample(model, n_tr, 40)).cuda()
+        Ytr, _ = U.fit(Xtr, n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=0, knn_mode=args.knn_mode)
+    else:
+        Xtr = torch.zeros((n_tr, 784), dtype=torch.float32, device="cuda")
+        Ytr = torch.zeros((n_tr, 2), dtype=torch.float32, device="cuda")
+    lo, hi = D.shard_range(n_q, rank, world)
+    chunks = []
+    for ch in range(lo // chunk, (hi + chunk - 1) // chunk):
+        c_lo, c_hi = ch * chunk, (ch + 1) * chunk
+        Xc = synth.lowrank_sample_device(model, chunk, 41 + ch)
+        a, b = max(lo, c_lo), min(hi, c_hi)
+        chunks.append((Xc[a - c_lo:b - c_lo].contiguous() if (a, b) != (c_lo, c_hi) else Xc, a))
+    kw = dict(n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=0, knn_mode=args.knn_mode)
+    ms = []
+    Yq = None
+    for i in range(warmup + steps):
+        Xb = Xtr.clone() if rank == 0 else torch.zeros_like(Xtr)
+        Yb = Ytr.clone() if rank == 0 else torch.zeros_like(Ytr)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record()
+        Yq = D.distributed_inference(Xb, Yb, chunks, n_q, **kw)
+        e1.record()
+        barrier()
+        if i >= warmup:
+            ms.append(e0.elapsed_time(e1))
+    t5 = maxr(sum(ms) / len(ms))
+    out["C5_distributed_inference"] = {
+        "workload": f"C5: model fitted on {n_tr}x784 (untimed), broadcast x{world}, umap_transform of {n_q}x784 "
+                    f"({n_q // world} rows per GPU in 1M-row chunks, {args.knn_mode} kNN, 67 epochs), all-gather",
+        "n_gpus": world, "ms": t5, "rows_per_s": n_q / (t5 / 1e3),
+        "broadcast_bytes": int((n_tr * 784 + n_tr * 2) * 4) if world > 1 else 0,
+        "allgather_bytes_per_rank": int(n_q * 2 * 4) if world > 1 else 0,
+        "sha1": sha(Yq), "steps": steps, "warmup": warmup}
+    del chunks, Yq
+    torch.cuda.empty_cache()
+    return out
 
 
 def _cpu_model():

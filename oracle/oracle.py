@@ -39,11 +39,11 @@ _I64, _I32, _F32, _F64, _U64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_float, c
 
 
 def build(force: bool = False) -> str:
-    """Compile the C oracle (gcc -O2 -ffp-contract=off, no fast-math)."""
+    """Compile the C oracle (gcc -O2 -ffp-contract=off -fopenmp, no fast-math)."""
     if _LIB_OVERRIDE:
         return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                                "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
@@ -55,6 +55,9 @@ def lib():
     global _lib
     if _lib is None:
         L = ctypes.CDLL(build())
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_threads.restype = None
+        L.oracle_get_threads.restype = ctypes.c_int
         L.oracle_philox4x32_10.argtypes = [_c_u32p, _c_u32p, _c_u32p]
         L.oracle_philox4x32_10.restype = None
         L.oracle_sqdist.argtypes = [_c_f32p, _c_f32p, _I32]
@@ -86,6 +89,15 @@ def lib():
         L.oracle_trust_from_penalty.restype = _F64
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads for the row-parallel loops (results do not depend on it)."""
+    lib().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 def _f32(a):

@@ -1,7 +1,7 @@
 /*
  * umap_oracle.c -- TEST INFRASTRUCTURE ONLY.
  *
- * A plain, slow, single-threaded CPU implementation of the GPU-UMAP hot path of
+ * A plain, slow CPU implementation of the GPU-UMAP hot path of
  * arXiv 2008.00325 ("Faster, Simpler and More Accurate: GPU-accelerated UMAP"),
  * written from the paper (PAPER.md, cited "P:<line>") and the readings fixed in
  * DESIGN.md §"Readings" (R1..R16).  Only tests/, __graft_entry__.smoke() and
@@ -9,9 +9,18 @@
  * no code, header or constant generator with the CUDA library under
  * paper_2008_00325_b200/.
  *
- * Compile: gcc -O2 -ffp-contract=off -fPIC -shared umap_oracle.c -lm
+ * Compile: gcc -O2 -ffp-contract=off -fopenmp -fPIC -shared umap_oracle.c -lm
  * (-ffp-contract=off: no FMA contraction; every fused multiply-add below is an
  *  explicit fmaf() call where the definition says so.)
+ *
+ * Threads: loops over rows whose results are independent of each other (kNN query
+ * rows, rho/sigma rows, membership rows, transform query rows, trust rows) are split
+ * over OpenMP threads; each row is still computed by one thread in the sequential order
+ * written below, and the only cross-row sum (the trust penalty) is an integer sum, so
+ * every output is bit-identical for any thread count (pinned by a test).  The layout SGD
+ * (oracle_optimize) stays single-threaded: its Hogwild mode is defined by the sequential
+ * order and its buffered mode sums in push order.  oracle_set_threads(n) overrides the
+ * OpenMP default (OMP_NUM_THREADS or all cores).
  *
  * Precision (task rule ③: fp64 unless the paper fixes it):
  *   - kNN distances: fp32, sequential fmaf over features.  The north_star fixes
@@ -27,9 +36,13 @@
  * fixed by the paper say "parity unpinned" below and in DESIGN.md.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+void oracle_set_threads(int n) { if (n > 0) omp_set_num_threads(n); }
+int oracle_get_threads(void) { return omp_get_max_threads(); }
 
 /* ------------------------------------------------------------------------- */
 /* Philox4x32-10 (Salmon et al., SC'11) -- the counter-based RNG used for the  */
@@ -87,39 +100,49 @@ static int key_less(float da, int64_t ia, float db, int64_t ib)
     return (da < db) || (da == db && ia < ib);
 }
 
+/* one query row x against all reference rows (self = the reference index excluded, or -1):   */
+/* insertion into the sorted list of the k smallest keys so far (best_d/best_i: scratch of k) */
+static void knn_row(const float* x, const float* Xr, int64_t nr, int32_t d, int32_t k, int64_t self,
+                    float* best_d, int64_t* best_i, int32_t* idx_out, float* dist_out)
+{
+    int cnt = 0;
+    for (int64_t j = 0; j < nr; ++j) {
+        if (j == self) continue;
+        float s = oracle_sqdist(x, Xr + j * (int64_t)d, d);
+        if (cnt < k) {
+            int p = cnt++;
+            while (p > 0 && key_less(s, j, best_d[p - 1], best_i[p - 1])) {
+                best_d[p] = best_d[p - 1]; best_i[p] = best_i[p - 1]; --p;
+            }
+            best_d[p] = s; best_i[p] = j;
+        } else if (key_less(s, j, best_d[k - 1], best_i[k - 1])) {
+            int p = k - 1;
+            while (p > 0 && key_less(s, j, best_d[p - 1], best_i[p - 1])) {
+                best_d[p] = best_d[p - 1]; best_i[p] = best_i[p - 1]; --p;
+            }
+            best_d[p] = s; best_i[p] = j;
+        }
+    }
+    for (int t = 0; t < k; ++t) {
+        idx_out[t] = t < cnt ? (int32_t)best_i[t] : -1;
+        dist_out[t] = t < cnt ? sqrtf(best_d[t]) : INFINITY;
+    }
+}
+
 int oracle_knn(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int32_t d, int32_t k,
                int64_t self_offset, int32_t* idx_out, float* dist_out)
 {
     if (k <= 0) return -1;
-    float* best_d = (float*)malloc(sizeof(float) * (size_t)k);
-    int64_t* best_i = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
-    for (int64_t i = 0; i < nq; ++i) {
-        int cnt = 0;
-        const float* x = Xq + i * (int64_t)d;
-        for (int64_t j = 0; j < nr; ++j) {
-            if (self_offset >= 0 && j == i + self_offset) continue;
-            float s = oracle_sqdist(x, Xr + j * (int64_t)d, d);
-            /* insertion into the sorted list of the k smallest keys so far */
-            if (cnt < k) {
-                int p = cnt++;
-                while (p > 0 && key_less(s, j, best_d[p - 1], best_i[p - 1])) {
-                    best_d[p] = best_d[p - 1]; best_i[p] = best_i[p - 1]; --p;
-                }
-                best_d[p] = s; best_i[p] = j;
-            } else if (key_less(s, j, best_d[k - 1], best_i[k - 1])) {
-                int p = k - 1;
-                while (p > 0 && key_less(s, j, best_d[p - 1], best_i[p - 1])) {
-                    best_d[p] = best_d[p - 1]; best_i[p] = best_i[p - 1]; --p;
-                }
-                best_d[p] = s; best_i[p] = j;
-            }
-        }
-        for (int t = 0; t < k; ++t) {
-            idx_out[i * k + t] = t < cnt ? (int32_t)best_i[t] : -1;
-            dist_out[i * k + t] = t < cnt ? sqrtf(best_d[t]) : INFINITY;
-        }
+#pragma omp parallel
+    {
+        float* best_d = (float*)malloc(sizeof(float) * (size_t)k);
+        int64_t* best_i = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < nq; ++i)
+            knn_row(Xq + i * (int64_t)d, Xr, nr, d, k, self_offset >= 0 ? i + self_offset : -1, best_d, best_i,
+                    idx_out + i * k, dist_out + i * k);
+        free(best_d); free(best_i);
     }
-    free(best_d); free(best_i);
     return 0;
 }
 
@@ -136,6 +159,7 @@ int oracle_knn(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int32_t
 int oracle_smooth_knn(const float* dist, int64_t n, int32_t k, float* rho_out, float* sigma_out)
 {
     const double target = log2((double)k);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         const float* row = dist + i * (int64_t)k;
         float rho = 0.0f;
@@ -175,6 +199,7 @@ int oracle_smooth_knn(const float* dist, int64_t n, int32_t k, float* rho_out, f
 int oracle_membership(const float* dist, const float* rho, const float* sigma,
                       int64_t n, int32_t k, float* w_out)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         for (int j = 0; j < k; ++j) {
             double delta = (double)dist[i * k + j] - (double)rho[i];
@@ -377,6 +402,7 @@ int oracle_optimize(const int64_t* indptr, const int32_t* col, const float* w, i
 int oracle_transform_init(const int32_t* idx, const float* w, int64_t nq, int32_t k,
                           const float* Ytr, int32_t dim, float* Yq)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t q = 0; q < nq; ++q) {
         for (int c = 0; c < dim; ++c) {
             double num = 0.0, den = 0.0;
@@ -404,11 +430,14 @@ int oracle_transform_optimize_range(const int32_t* idx, const float* w, int64_t 
     float w_max = 0.0f;
     for (int64_t p = 0; p < nq * k; ++p) if (w[p] > w_max) w_max = w[p];
     if (w_max <= 0.0f) return 0;
-    double* g = (double*)malloc(sizeof(double) * (size_t)dim);
     if (e_begin < 1) e_begin = 1;
     if (e_end > n_epochs_t) e_end = n_epochs_t;
     for (int32_t e = e_begin; e < e_end; ++e) {
         float alpha = alpha0 * (1.0f - (float)e / (float)n_epochs_t);
+#pragma omp parallel
+        {
+        double* g = (double*)malloc(sizeof(double) * (size_t)dim);
+#pragma omp for schedule(static)
         for (int64_t q = 0; q < nq; ++q) {
             float* yq = Yq + q * dim;
             uint32_t head = (uint32_t)(q + q_offset);
@@ -441,8 +470,9 @@ int oracle_transform_optimize_range(const int32_t* idx, const float* w, int64_t 
                 }
             }
         }
+        free(g);
+        }
     }
-    free(g);
     return 0;
 }
 
@@ -467,12 +497,17 @@ int oracle_transform_optimize(const int32_t* idx, const float* w, int64_t nq, in
 int64_t oracle_trust_penalty(const float* X, int32_t d, const float* Y, int32_t dy, int64_t n,
                              int32_t k, int64_t row_begin, int64_t row_end, int64_t* row_pen)
 {
+    int64_t S = 0;
+#pragma omp parallel reduction(+ : S)
+    {
     int32_t* nn = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
     float* nd = (float*)malloc(sizeof(float) * (size_t)k);
+    float* bd = (float*)malloc(sizeof(float) * (size_t)k);
+    int64_t* bi = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
     float* dx = (float*)malloc(sizeof(float) * (size_t)n);
-    int64_t S = 0;
+#pragma omp for schedule(dynamic, 4)
     for (int64_t i = row_begin; i < row_end; ++i) {
-        oracle_knn(Y + i * dy, 1, Y, n, dy, k, i, nn, nd);
+        knn_row(Y + i * dy, Y, n, dy, k, i, bd, bi, nn, nd);
         for (int64_t l = 0; l < n; ++l) dx[l] = oracle_sqdist(X + i * (int64_t)d, X + l * (int64_t)d, d);
         int64_t pen = 0;
         for (int t = 0; t < k; ++t) {
@@ -487,7 +522,8 @@ int64_t oracle_trust_penalty(const float* X, int32_t d, const float* Y, int32_t 
         if (row_pen) row_pen[i - row_begin] = pen;
         S += pen;
     }
-    free(nn); free(nd); free(dx);
+    free(nn); free(nd); free(bd); free(bi); free(dx);
+    }
     return S;
 }
 

@@ -45,10 +45,11 @@ def _default_merge():
     return api.topk_merge
 
 
-def sharded_knn(X, k, group=None, knn_fn=None, merge_fn=None):
+def sharded_knn(X, k, group=None, knn_fn=None, merge_fn=None, phase_mark=None):
     """Exact kNN of every row of X against X (self excluded), reference rows sharded
     across the ranks of `group`.  Returns (idx int32 n x k, dist fp32 n x k), identical
-    on every rank."""
+    on every rank.  phase_mark (optional): called with "searched" and "gathered" at the
+    phase boundaries (bench.py records CUDA events there)."""
     knn_fn = knn_fn or _default_knn()
     merge_fn = merge_fn or _default_merge()
     rank, world = _rank_world(group)
@@ -57,12 +58,18 @@ def sharded_knn(X, k, group=None, knn_fn=None, merge_fn=None):
     if hi - lo < k + 1:
         raise ValueError(f"shard of {hi - lo} rows is too small for k={k}")
     ci, cd = knn_fn(X, X[lo:hi], k, exclude_self=True, query_offset=0, index_offset=lo, squared=True)
+    if phase_mark:
+        phase_mark("searched")
     if world == 1:
+        if phase_mark:
+            phase_mark("gathered")
         return merge_fn(ci[None], cd[None], k)
     gi = [torch.empty_like(ci) for _ in range(world)]
     gd = [torch.empty_like(cd) for _ in range(world)]
     dist.all_gather(gi, ci.contiguous(), group=group)
     dist.all_gather(gd, cd.contiguous(), group=group)
+    if phase_mark:
+        phase_mark("gathered")
     return merge_fn(torch.stack(gi), torch.stack(gd), k)
 
 
@@ -140,3 +147,35 @@ def partitioned_transform(X_train, Y_train, Xq_local, q_offset, n_total, group=N
     dist.all_gather(parts, pad, group=group)
     out = [parts[r][:shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]] for r in range(world)]
     return torch.cat(out)
+
+
+def distributed_inference(X_train, Y_train, chunks, n_total, group=None, transform_fn=None, src=0, **kw):
+    """The paper's distributed UMAP inference (App. B): the model (X_train, Y_train)
+    trained on rank `src` is broadcast, every rank embeds its partition -- a list of
+    (Xq_chunk, q_offset) with global query ids, whose chunks together cover shard_range(n_total,
+    rank, world) in order -- and the partitions are all-gathered (every rank gets n_total rows).
+    Bit-identical for any world size: each query row depends only on the model and its global
+    id (R15)."""
+    if transform_fn is None:
+        from . import api
+        transform_fn = api.transform
+    broadcast_model(X_train, Y_train, group=group, src=src)
+    rank, world = _rank_world(group)
+    lo, hi = shard_range(n_total, rank, world)
+    parts = []
+    nxt = lo
+    for Xq, off in chunks:
+        assert off == nxt, "chunks must cover the rank's shard in order"
+        parts.append(transform_fn(X_train, Y_train, Xq, q_offset=off, **kw))
+        nxt = off + Xq.shape[0]
+    assert nxt == hi, "chunks must cover the rank's shard"
+    Yq = torch.cat(parts) if len(parts) > 1 else parts[0]
+    if world == 1:
+        return Yq
+    m = max(shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0] for r in range(world))
+    pad = torch.zeros((m, Yq.shape[1]), dtype=Yq.dtype, device=Yq.device)
+    pad[:Yq.shape[0]] = Yq
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad, group=group)
+    return torch.cat([out[r][:shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]]
+                      for r in range(world)])

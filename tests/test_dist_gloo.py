@@ -106,7 +106,14 @@ def _worker(rank, world, port, q):
         lo, hi = D.shard_range(160, rank, world)
         Yq = D.partitioned_transform(Xtr, Ytr, torch.from_numpy(Xall[100 + lo:100 + hi]), lo, 160,
                                      transform_fn=transform_cpu)
-        q.put((rank, idx.numpy(), dd.numpy(), S, Yq.numpy()))
+        # bench.py's C5 leg: the same inference through distributed_inference, the rank's shard in
+        # two chunks with global query ids (the model is re-broadcast from rank 0)
+        Xtr2 = torch.from_numpy(Xall[:100]) if rank == 0 else torch.zeros((100, 6))
+        Ytr2 = torch.from_numpy(synth.uniform_embedding(100, 2, seed=4)) if rank == 0 else torch.zeros((100, 2))
+        mid = (lo + hi) // 2
+        chunks = [(torch.from_numpy(Xall[100 + lo:100 + mid]), lo), (torch.from_numpy(Xall[100 + mid:100 + hi]), mid)]
+        Yq2 = D.distributed_inference(Xtr2, Ytr2, chunks, 160, transform_fn=transform_cpu)
+        q.put((rank, idx.numpy(), dd.numpy(), S, Yq.numpy(), Yq2.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -132,11 +139,12 @@ def test_gloo_world2_matches_single_process():
     Xall = synth.lowrank(260, 6, blobs=3, seed=3)
     Ytr = synth.uniform_embedding(100, 2, seed=4)
     Yq_ref = O.transform(Xall[:100], Ytr, Xall[100:], k=10, n_epochs=30, a=1.5769434603, b=0.8950608779, seed=5)
-    for rank, idx, dd, S, Yq in res:
+    for rank, idx, dd, S, Yq, Yq2 in res:
         assert np.array_equal(idx, ri), rank
         assert np.array_equal(dd, rd), rank
         assert S == S_ref
         assert np.array_equal(Yq, Yq_ref)
+        assert np.array_equal(Yq2, Yq_ref)
 
 
 def test_shard_ranges_cover_rows():

@@ -492,3 +492,36 @@ def test_spectral_init_matches_dense_eigensolver():
         v = V[:, j]
         lj = v @ L @ v / (v @ v)
         assert np.linalg.norm(L @ v - lj * v) <= 1e-3 * np.linalg.norm(v)
+
+
+def test_row_parallel_loops_are_thread_invariant(O):
+    """The OpenMP row loops (kNN, rho/sigma, membership, transform, trust) give bit-identical
+    results at 1 and at all threads: each row is one thread's sequential computation and the
+    only cross-row sum is an integer one."""
+    X = synth.lowrank(700, 24, blobs=5, seed=12)
+    Xq = synth.lowrank(300, 24, blobs=5, seed=13)
+    Y = synth.lowrank(700, 2, blobs=5, seed=14)
+    A_, B_ = 1.5769434603, 0.8950608779
+    out = []
+    n_all = O.get_threads()
+    for th in (1, max(2, n_all)):
+        O.set_threads(th)
+        try:
+            idx, dist = O.knn(X, X, 15, self_offset=0)
+            rho, sigma = O.smooth_knn(dist)
+            w = O.membership(dist, rho, sigma)
+            S = O.trust_penalty(X, Y, 7)
+            qi, qd = O.knn(Xq, X, 15)
+            qr, qs = O.smooth_knn(qd)
+            qw = O.membership(qd, qr, qs)
+            Yq = O.transform_init(qi, qw, Y)
+            Yq = O.transform_optimize(qi, qw, Y, Yq, A_, B_, 30, m=5, seed=3)
+            out.append((idx, dist, rho, sigma, w, S, Yq))
+        finally:
+            O.set_threads(n_all)
+    def same(a, b):
+        if isinstance(a, (tuple, list)):
+            return len(a) == len(b) and all(same(x, y) for x, y in zip(a, b))
+        return np.array_equal(np.asarray(a), np.asarray(b))
+    for a, b in zip(*out):
+        assert same(a, b)

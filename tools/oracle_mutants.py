@@ -51,7 +51,7 @@ def main():
         c = os.path.join(tmp, f"m{i}.c")
         so = os.path.join(tmp, f"m{i}.so")
         open(c, "w").write(mut)
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", so, c, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-o", so, c, "-lm"])
         env = dict(os.environ, UMAP_ORACLE_LIB=so)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "not gpu", "-p", "no:cacheprovider", *PINS],
                            cwd=ROOT, env=env, capture_output=True, text=True)
