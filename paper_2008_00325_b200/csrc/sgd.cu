@@ -968,7 +968,10 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
         while (b < nb) {
             int bn = 0;
             if (lane == 0) bn = atomicAdd(&s_batch, 1);
-            const int j = 32 * b + lane;
+            // batch b takes list entries b, b + nb, b + 2 nb, ...: the list is in CSR order (equal
+            // heads adjacent), so a strided batch has 32 different heads and its shared-memory
+            // reductions do not serialise on one address (9.3 -> ~1 wavefront per ATOMS)
+            const int j = b + lane * nb;
             const bool act = j < nl;
             const uint32_t ent = act ? list[j] : 0u;
             const int hl = (int)(ent >> 21), t = act ? (int)(ent & 0x1FFFFFu) : v_lo;

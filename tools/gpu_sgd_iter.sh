@@ -1,7 +1,7 @@
 #!/bin/bash
 # SGD iteration on the GPU box: SGD parity tests, launch-shape bit-identity, bench (kernel split).
 # usage: bash tools/gpu_sgd_iter.sh <tag> [pytest -k expr]
-TAG=${1:-x}; K=${2:-"sgd or optimize or fit or hogwild"}
+TAG=${1:-x}; K=${2:-"(sgd or optimize or fit or hogwild) and not c2_full"}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x -k "$K" 2>&1 | tail -5 > gpurun_out/pytest_sgd_${TAG}.log
 for vt in 0 256 700; do
