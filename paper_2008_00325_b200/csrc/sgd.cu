@@ -52,6 +52,7 @@ struct SgdArgs {
     const int* max_row;      // flat2/3: device max CSR row length (> 65535: 64-bit CAS accumulation)
     int list_cap;            // flat3: due-list capacity (>= every CTA's record count)
     int scan_split_pct;      // flat3: % of the next epoch's scan done before the grid barrier's arrive
+    int batch_static;        // flat3: 1 = warp w takes batches w, w + 32, ... (0: claimed dynamically)
 };
 
 __device__ __forceinline__ u32x4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const SgdArgs& A)
@@ -961,13 +962,20 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
         const uint32_t* list = list0 + (size_t)buf * cap;
         const int nl = s_nlist;
         const int nb = (nl + 31) >> 5;
-        // B(epoch): the next batch is claimed before the current one is processed
-        int b = 0;
-        if (lane == 0) b = atomicAdd(&s_batch, 1);
-        b = __shfl_sync(0xffffffffu, b, 0);
+        // B(epoch): warp w takes batches w, w + 32, ... (batch_static, the default: 7 % faster than
+        // claiming them from a shared counter, the next one before the current one is processed;
+        // a software-pipelined variant that preps the next batch's gathers before the current
+        // batch's arithmetic measured slower: 8.3-9.0 vs 8.0-8.1 ms)
+        const int warp = threadIdx.x >> 5;
+        constexpr int NW = 32;
+        int b = warp;
+        if (!A.batch_static) {
+            if (lane == 0) b = atomicAdd(&s_batch, 1);
+            b = __shfl_sync(0xffffffffu, b, 0);
+        }
         while (b < nb) {
-            int bn = 0;
-            if (lane == 0) bn = atomicAdd(&s_batch, 1);
+            int bn = b + NW;
+            if (!A.batch_static && lane == 0) bn = atomicAdd(&s_batch, 1);
             // batch b takes list entries b, b + nb, b + 2 nb, ...: the list is in CSR order (equal
             // heads adjacent), so a strided batch has 32 different heads and its shared-memory
             // reductions do not serialise on one address (9.3 -> ~1 wavefront per ATOMS)
@@ -978,7 +986,7 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
             int qa[DIM];
             edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, hl, t, act, qa);
             if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
-            b = __shfl_sync(0xffffffffu, bn, 0);
+            b = A.batch_static ? bn : __shfl_sync(0xffffffffu, bn, 0);
         }
         // A(epoch + 1), first part: fills the tail of B(epoch)
         if (epoch + 1 < A.e_end) scan(epoch + 1, buf ^ 1, split);
@@ -1322,6 +1330,8 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
             A.list_cap = cap;
             const char* e = getenv("UMAP_SGD_SCAN_SPLIT");  // tuning knob (% of the scan before the barrier)
             A.scan_split_pct = e ? std::max(0, std::min(100, atoi(e))) : 50;
+            const char* bs = getenv("UMAP_SGD_BATCH_STATIC");  // tuning knob (1: measured 7 % faster)
+            A.batch_static = bs ? atoi(bs) : 1;
         } else {
             ver = 2;
         }
@@ -1340,7 +1350,9 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
         const size_t per_v = (sizeof(unsigned long long) + (ver == 2 ? sizeof(float) : 0)) * (size_t)DIM;
         smem = per_v * A.vt + QBYTES;
     }
-    auto kern = ver == 3 ? sgd_flat3_kernel<DIM, MC> : ver == 2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
+    const int nt = 1024;
+    auto kern = ver == 3 ? sgd_flat3_kernel<DIM, MC>
+            : ver == 2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
     static PerDeviceOnce attr[4];
     if (attr[ver].first()) {
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1348,7 +1360,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
                                            (int)cudaSharedmemCarveoutMaxL1));
     }
     int per_sm = 0;
-    UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, smem));
+    UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem));
     if (per_sm < 1) {
         set_last_error("SGD kernel does not fit one CTA per SM");
         return UMAP_ERR_CUDA;
@@ -1368,7 +1380,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
     }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
-    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(1024), args, smem, s));
+    UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(nt), args, smem, s));
     UMAP_LAUNCH_CHECK(ver == 3 ? "sgd_flat3_kernel" : ver == 2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
     return UMAP_OK;
 }
