@@ -94,6 +94,11 @@ typedef struct {
     float    unknown_dist;         /* a label -1 on either end -> x exp(-unknown_dist), 1.0  */
     int32_t  init;                 /* a7: 0 = random U[-10,10) (R11), 1 = spectral (R18)     */
     int32_t  spectral_iters;       /* block power iterations of the spectral init, 0 -> 300  */
+    int32_t  transform_precision;  /* a9 per-edge arithmetic of umap_transform(_optimize):    */
+                                   /* 0 = fp32 with MUFU pow/rcp (default, fast); 1 = fp64   */
+                                   /* with IEEE pow and division, position stored in fp32    */
+                                   /* after every update (R15's oracle reading: equal to the */
+                                   /* oracle bit for bit, ~8x slower on the C5 transform)    */
 } umap_params;
 
 /* Per-stage device times (ms, CUDA events on `stream`) and graph statistics. */

@@ -30,7 +30,8 @@ class UmapParams(ctypes.Structure):
                 ("negative_sample_rate", c_int32), ("learning_rate", c_float), ("repulsion_strength", c_float),
                 ("a", c_float), ("b", c_float), ("seed", c_uint64), ("sgd_mode", c_int32), ("knn_mode", c_int32),
                 ("knn_candidates", c_int32), ("transform_epochs", c_int32), ("trust_k", c_int32),
-                ("far_dist", c_float), ("unknown_dist", c_float), ("init", c_int32), ("spectral_iters", c_int32)]
+                ("far_dist", c_float), ("unknown_dist", c_float), ("init", c_int32), ("spectral_iters", c_int32),
+                ("transform_precision", c_int32)]
 
 
 class UmapFitStats(ctypes.Structure):

@@ -57,7 +57,7 @@ def _any(t, dtype, name):
 def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0, negative_sample_rate=5,
            learning_rate=1.0, repulsion_strength=1.0, a=0.0, b=0.0, seed=0, sgd_mode="deterministic",
            knn_mode="exact", knn_candidates=32, transform_epochs=0, trust_k=0, far_dist=5.0,
-           unknown_dist=1.0, init="random", spectral_iters=0) -> UmapParams:
+           unknown_dist=1.0, init="random", spectral_iters=0, transform_precision="fp32") -> UmapParams:
     p = UmapParams()
     _lib.load().umap_params_default(ctypes.byref(p))
     p.n_neighbors, p.n_components, p.n_epochs = n_neighbors, n_components, n_epochs
@@ -70,6 +70,8 @@ def params(n_neighbors=15, n_components=2, n_epochs=0, min_dist=0.1, spread=1.0,
     p.far_dist, p.unknown_dist = far_dist, unknown_dist
     p.init = {"random": 0, "spectral": 1}[init] if isinstance(init, str) else init
     p.spectral_iters = spectral_iters
+    p.transform_precision = {"fp32": 0, "fp64": 1}[transform_precision] if isinstance(transform_precision, str) \
+        else transform_precision
     return p
 
 

@@ -261,6 +261,10 @@ umap_status check_params(const umap_params* p)
         set_last_error("init must be 0 (random) or 1 (spectral)");
         return UMAP_ERR_INVALID_ARGUMENT;
     }
+    if (p->transform_precision != 0 && p->transform_precision != 1) {
+        set_last_error("transform_precision must be 0 (fp32) or 1 (fp64)");
+        return UMAP_ERR_INVALID_ARGUMENT;
+    }
     // R13: a due edge's fixed-point contributions (2 q(g_att) + sum of m q(g_rep), each |q| <=
     // 4 alpha 2^24) are summed in int32 before the segment sums widen to int64
     if (p->sgd_mode == UMAP_SGD_DETERMINISTIC &&
@@ -407,6 +411,7 @@ void umap_params_default(umap_params* p)
     p->unknown_dist = 1.0f;
     p->init = 0;
     p->spectral_iters = 0;
+    p->transform_precision = 0;
 }
 
 // R8: Levenberg-Marquardt least squares of Phi(x) = 1/(1 + a x^{2b}) against the

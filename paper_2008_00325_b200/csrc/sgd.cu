@@ -1158,7 +1158,43 @@ __global__ void random_init_kernel(int64_t n, int dim, uint32_t k0, uint32_t k1,
 // Thread per query row; all epochs in one launch (rows are independent: P:138 only
 // the query rows move, the training layout is frozen), so there is no inter-epoch
 // barrier and no atomics.  Deterministic by construction.
-template <int DIM, int KMAX>
+// F64: the per-edge arithmetic of R12/R15 in fp64 with the position stored back in fp32 after
+// every update (the oracle's precision reading, R15): coefficients -2ab s^(b-1) /
+// (a s^b + 1) and 2 gamma b / ((0.001 + s)(a s^b + 1)) with IEEE pow and division, products and
+// sums in the written order without FMA contraction (measured: equal to the oracle bit for bit,
+// teacher-forced; ~8x slower on the C5 transform, an exp2(b log2 s) form in fp64 slower still).
+// !F64 (the default): the fp32 MUFU form of the fit SGD.
+template <int DIM>
+__device__ __forceinline__ void transform_update_f64(float (&y)[DIM], const float (&yo)[DIM], bool attractive,
+                                                     double a, double b, double gamma, double alpha)
+{
+    double df[DIM], s = 0.0;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        df[c] = __dsub_rn((double)y[c], (double)yo[c]);
+        s = __dadd_rn(s, __dmul_rn(df[c], df[c]));
+    }
+    double g[DIM];
+    if (attractive) {
+        double coef = 0.0;
+        if (s > 0.0)
+            coef = __ddiv_rn(__dmul_rn(__dmul_rn(-2.0 * a, b), pow(s, b - 1.0)), __dadd_rn(__dmul_rn(a, pow(s, b)), 1.0));
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) g[c] = __dmul_rn(fmin(fmax(__dmul_rn(coef, df[c]), -4.0), 4.0), alpha);
+    } else if (s > 0.0) {
+        const double cr = __ddiv_rn(__dmul_rn(2.0 * gamma, b),
+                                    __dmul_rn(__dadd_rn(0.001, s), __dadd_rn(__dmul_rn(a, pow(s, b)), 1.0)));
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) g[c] = __dmul_rn(fmin(fmax(__dmul_rn(cr, df[c]), -4.0), 4.0), alpha);
+    } else {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) g[c] = __dmul_rn(4.0, alpha);
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) y[c] = __double2float_rn(__dadd_rn((double)y[c], g[c]));
+}
+
+template <int DIM, int KMAX, bool F64>
 __global__ void __launch_bounds__(128)
 transform_sgd_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w, int64_t nq, int k,
                      const float* __restrict__ Ytr, int64_t ntr, float* __restrict__ Yq, const float* w_max_p,
@@ -1203,6 +1239,19 @@ transform_sgd_kernel(const int32_t* __restrict__ idx, const float* __restrict__ 
             const int64_t t = tt[j];
             float yt[DIM], g[DIM];
             load_row<DIM>(Ytr, t, yt);
+            if constexpr (F64) {
+                transform_update_f64<DIM>(y, yt, true, (double)a, (double)b, (double)gamma, (double)alpha);
+                u32x4 rnd = {0, 0, 0, 0};
+                for (int p = 0; p < m; ++p) {
+                    if ((p & 3) == 0) rnd = philox4x32_10(head, (uint32_t)t, (uint32_t)e, (uint32_t)(p >> 2), key0, key1);
+                    const uint32_t u = pick(rnd, p & 3);
+                    const int64_t v = (int64_t)(((unsigned long long)u * (unsigned long long)ntr) >> 32);
+                    float yv[DIM];
+                    load_row<DIM>(Ytr, v, yv);
+                    transform_update_f64<DIM>(y, yv, false, (double)a, (double)b, (double)gamma, (double)alpha);
+                }
+                continue;
+            }
             float s = 0.0f;
 #pragma unroll
             for (int c = 0; c < DIM; ++c) { const float df = y[c] - yt[c]; s = fmaf(df, df, s); }
@@ -1442,7 +1491,8 @@ umap_status launch_transform_t(const int32_t* idx, const float* w, int64_t nq, i
                                int64_t q_offset, int init, cudaStream_t s)
 {
     ProfScope ps(PROF_TRANSFORM_SGD, s);
-    transform_sgd_kernel<DIM, KMAX><<<ceil_div(nq, 128), 128, 0, s>>>(
+    auto kern = p->transform_precision == 1 ? transform_sgd_kernel<DIM, KMAX, true> : transform_sgd_kernel<DIM, KMAX, false>;
+    kern<<<ceil_div(nq, 128), 128, 0, s>>>(
         idx, w, nq, k, Ytr, ntr, Yq, wmax, p->a, p->b, p->repulsion_strength, p->learning_rate, nt, eb, ee,
         p->negative_sample_rate, (uint32_t)p->seed, (uint32_t)(p->seed >> 32), q_offset, init);
     UMAP_LAUNCH_CHECK("transform_sgd_kernel");
