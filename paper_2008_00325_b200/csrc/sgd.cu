@@ -1,22 +1,27 @@
 // sgd.cu -- random init (a7), SGD layout (a6, a8) and transform SGD (a9).
 //
-// Layout SGD.  One launch per epoch e (1 <= e < N).
-// A warp owns 32 consecutive vertices (their CSR rows are contiguous): it streams
-// the rows' (col, w) pairs with coalesced loads, evaluates the closed-form schedule
-// (R9) per edge, compacts the due edges into a per-warp shared-memory queue and
-// processes the queue 32 items at a time, so every lane carries a due edge while
-// the expensive part runs (attractive term + m negatives + 2 Philox calls).
+// Layout SGD: all epochs in one cooperative launch, a grid barrier between
+// epochs.  A CTA owns a cost-balanced vertex range; the due edges of an epoch (closed-form
+// schedule, R9) are compacted so that every lane carries a due edge through the expensive part
+// (attractive term + m negatives + 2 Philox calls).
 //
-//  * DETERMINISTIC (R13): reads Y_e only, writes Y_{e+1} (ping-pong).  Each
-//    vertex is updated only by the warp that owns it ("owner computes"): because
-//    B is bit-exactly symmetric, the tail update of edge (i,j) equals the head
-//    update of edge (j,i), so vertex i receives 2 q(g_att) per own due edge plus
-//    q(g_rep) per negative, q(g) = round(g 2^32) summed in int64 (order-free, so the
-//    result is identical for any launch configuration).  No global atomics.
-//  * HOGWILD: in-place.  Each due edge reads the live positions, moves
-//    its head in registers through the attractive and the m repulsive updates
-//    (the paper's register accumulation) and pushes -g_att to the tail and
-//    the accumulated head delta with fp32 vector atomics.
+//  * DETERMINISTIC (R13): reads Y_e only, writes Y_{e+1} (ping-pong).  Each vertex is
+//    updated only by the CTA that owns it ("owner computes"): because B is bit-exactly symmetric,
+//    the tail update of edge (i,j) equals the head update of edge (j,i), so vertex i receives
+//    2 q(g_att) per own due edge plus q(g_rep) per negative, q(g) = round(g 2^24) per term, the
+//    terms of a due edge summed in int32 and added to the head's shared-memory accumulator by
+//    32-bit reductions of the sum split at bit 16 (flat2 / flat3) or by 64-bit warp-segment sums
+//    (the round-1 flat kernel) -- integer sums, so the result is identical for any launch shape
+//    and work order.  No global atomics.  Kernels: sgd_flat3_kernel (default: the whole CTA range
+//    in one piece, per-epoch due lists), sgd_flat2_kernel (pieces of vt vertices, e.g. C4),
+//    sgd_flat_kernel (round 1, UMAP_SGD_VARIANT=100), sgd_persistent_kernel (DIM 8 / 16).
+//  * HOGWILD: in-place.  Each due edge reads the live positions, moves its head in
+//    registers through the attractive and the m repulsive updates (the paper's register
+//    accumulation) and pushes -g_att to the tail and the accumulated head delta with fp32
+//    vector atomics.
+// Position gathers go through L1 (ld.global.ca): within an epoch the deterministic kernels read
+// only the ping-pong buffer Y_e, and the grid barrier's acquire invalidates L1 before the next
+// epoch; Hogwild reads are unsynchronised by definition (staleness bounded to one epoch).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -89,8 +94,7 @@ __device__ __forceinline__ bool edge_due_f(float r, float ef, float ef1)
     return floorf(__fmul_rn(ef, r)) > floorf(__fmul_rn(ef1, r));
 }
 
-// positions are read through L2 only (ld.global.cg): they change between epochs of the
-// persistent kernel and L1 is not coherent
+// L2-only read (ld.global.cg): the transform's training rows and the piece setup
 template <int DIM>
 __device__ __forceinline__ void load_row(const float* Y, int64_t v, float (&y)[DIM])
 {
@@ -163,7 +167,8 @@ constexpr int SGD_WARPS = 8;  // warps per CTA at MINB = 4; in general 32 / MINB
 template <int MINB> constexpr int sgd_warps() { return MINB >= 4 ? SGD_WARPS : 32 / MINB; }
 constexpr int QCAP = 64;
 
-// R13 fixed point: q(g) = round(g 2^24) (exact scaling, |g| <= 4 so |q| <= 2^26 fits int32)
+// R13 fixed point: q(g) = round(g 2^24) (exact scaling; |g| <= 4 alpha, so |q| <= 2^26 alpha0; a
+// due edge's (2 + m) terms fit int32 while (2 + m) alpha0 < 32, enforced by check_params)
 __device__ __forceinline__ int qfix(float g) { return __float2int_rn(g * 16777216.0f); }
 
 // One due edge (h, t) at epoch e: attractive update of h (and, Hogwild, t) and M negative
