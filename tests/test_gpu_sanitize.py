@@ -1,0 +1,33 @@
+"""compute-sanitizer memcheck and synccheck over one tiny invocation of every kernel family
+(tools/sanitize_run.py): no out-of-bounds or misaligned access, no illegal barrier use, on the
+B200 (pytest -m gpu).  racecheck / initcheck and every SGD variant: tools/sanitize.sh,
+profiles/sanitize_r02/."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CS = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(CS) and not shutil.which("compute-sanitizer"):
+        pytest.fail("compute-sanitizer not found")
+    env = dict(os.environ, SAN_N="400", SAN_EPOCHS="6")
+    r = subprocess.run([CS if os.path.exists(CS) else "compute-sanitizer", "--tool", tool, "--print-limit", "10",
+                        sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")],
+                       capture_output=True, text=True, env=env, timeout=1200)
+    out = r.stdout + r.stderr
+    assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]
+    assert "\nok" in out
