@@ -1481,10 +1481,12 @@ template <int DIM>
 umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
 {
     const int sv = sgd_variant();
-    if (DIM <= 4 && det && (sv == 0 || sv == 100 || sv == 101)) {  // DIM 8, 16: 64 registers per thread spill
-        // 100: the round-1 flat kernel, 101: flat2 (A/B comparisons); default flat3 (else flat2)
-        const int ver = sv == 100 ? 1 : sv == 101 ? 2 : 3;
-        return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver);
+    if constexpr (DIM <= 4) {  // DIM 8, 16: 64 registers per thread spill (persistent chunk kernel)
+        if (det && (sv == 0 || sv == 100 || sv == 101)) {
+            // 100: the round-1 flat kernel, 101: flat2 (A/B comparisons); default flat3 (else flat2)
+            const int ver = sv == 100 ? 1 : sv == 101 ? 2 : 3;
+            return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver);
+        }
     }
     if (A.m == 5) return det ? launch_sgd_m<DIM, true, 5>(A, s) : launch_sgd_m<DIM, false, 5>(A, s);
     return det ? launch_sgd_m<DIM, true, 0>(A, s) : launch_sgd_m<DIM, false, 0>(A, s);

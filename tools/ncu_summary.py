@@ -6,6 +6,8 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", 
      "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
      "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
      "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+     "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",  # tcgen05 tensor pipe busy
+     "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
      "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_elapsed",
      "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
      "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
@@ -30,11 +32,12 @@ for r in rows[2:]:
     name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("umapb200::", "").replace("<unnamed>::", "")
     rec = {}
     for m in M:
-        if m in d:
+        col = m if m in d else next((c for c in d if c.endswith("." + m)), None)  # section-prefixed names
+        if col is not None:
             try:
-                rec[m] = float(d[m].replace(",", "")) * SCALE.get(units.get(m, ""), 1)
+                rec[m] = float(d[col].replace(",", "")) * SCALE.get(units.get(col, ""), 1)
             except ValueError:
-                rec[m] = d[m]
+                rec[m] = d[col]
     if "dram__bytes_read.sum" in rec:
         rec["dram_bytes_per_launch"] = rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
     key = name
@@ -46,4 +49,4 @@ json.dump(res, open(out, "w"), indent=1)
 for k, v in res["kernels"].items():
     print(f"{k[:48]:48s} {v.get('gpu__time_duration.sum', 0) / 1e6:9.3f} ms  dram {v.get('dram_bytes_per_launch', 0) / 1e6:9.1f} MB"
           f"  L2 {v.get('lts__t_sectors.sum', 0) * 32 / 1e9:7.2f} GB  sm {v.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):5.1f}%"
-          f"  tensor {v.get('sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed', '-')}")
+          f"  tensor pipe {v.get('sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed', '-')}%")
