@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <vector>
 #include <cstdio>
+#include <algorithm>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -32,6 +33,7 @@
 namespace umapb200 {
 
 static thread_local int64_t g_last_rank_ambiguous = 0;
+static thread_local int64_t g_last_regrouped = 0;
 static thread_local double g_last_fine_fraction = 1.0;
 
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
@@ -242,6 +244,8 @@ struct TcArgs {
     const int32_t* tile_count;
     int tile_ld;
     uint8_t* flags;           // MODE 2 (coarse pass): flags[b * tile_ld + t] = 1 if tile t may matter
+    uint8_t* rowflags;        // MODE 2, optional: rowflags[q * tile_ld + t] = 1 if tile t may matter for row q
+    const int32_t* chunk_block;  // MODE 1, optional: query block of tile-list chunk c (hist / amb_count added atomically)
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
@@ -285,7 +289,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     const bool leader = rank == 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t q0 = (int64_t)blockIdx.x * TC_BM;
+    // chunked fine pass (chunk_block != nullptr): CTA pair c works on tile-list chunk c of the
+    // 256-row query block chunk_block[c]; chunks of one block run concurrently and add their counts
+    const int64_t q0 = a.chunk_block ? ((int64_t)a.chunk_block[blockIdx.x >> 1] * 2 + (blockIdx.x & 1)) * TC_BM
+                                     : (int64_t)blockIdx.x * TC_BM;
     const int64_t r_lo = (int64_t)blockIdx.y * a.split_len;
     const int64_t r_hi = imin64(a.nr, r_lo + a.split_len);
     const int ntiles_all = (int)((r_hi - r_lo + TC_BN - 1) / TC_BN);
@@ -481,7 +488,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         const bool act = (cm >> u) & 1u;
                         if (act && b_hi == b_lo && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
                         if (act && b_hi != b_lo) {
-                            if (n_amb < a.amb_cap) amb_row[n_amb] = (int32_t)(jb + u);
+                            const int pos = a.chunk_block ? atomicAdd(a.amb_count + q * NP + half, 1) : n_amb;
+                            if (pos < a.amb_cap) amb_row[pos] = (int32_t)(jb + u);
                             ++n_amb;
                         }
                     }
@@ -508,7 +516,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const bool amb = has && b_hi != b_lo;
                     if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
                     if (amb) {
-                        if (n_amb < a.amb_cap) amb_row[n_amb] = (int32_t)(jb + u);
+                        const int pos = a.chunk_block ? atomicAdd(a.amb_count + q * NP + half, 1) : n_amb;
+                        if (pos < a.amb_cap) amb_row[pos] = (int32_t)(jb + u);
                         ++n_amb;
                     }
                 }
@@ -526,10 +535,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 int sum = 0;
 #pragma unroll
                 for (int pp = 0; pp < NP; ++pp) sum += Hs[(pp * TC_KT + t) * TC_BM + row];
-                a.hist[q * k + t] = sum;
+                if (a.chunk_block) {
+                    if (sum) atomicAdd(a.hist + q * k + t, sum);
+                } else {
+                    a.hist[q * k + t] = sum;
+                }
             }
         }
-        if (valid) a.amb_count[q * NP + half] = n_amb;
+        if (valid && !a.chunk_block) a.amb_count[q * NP + half] = n_amb;
     } else if constexpr (MODE == 2) {
         // ---------------------------------------------------- coarse tile flags (warps 2..9)
         // Single-BF16 pass over the hi operands (norms folded: accumulator = -d2~/2, error
@@ -569,6 +582,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
             tc_fence_before();
             __syncwarp();
+            if (a.rowflags && hit) a.rowflags[q * a.tile_ld + tile] = 1;  // both column halves may store 1
             if (__any_sync(0xffffffffu, hit) && lane == 0) a.flags[(int64_t)pblk * a.tile_ld + tile] = 1;
             if (lane == 0) {
                 if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(tempty0 + 8 * b, 0));
@@ -1230,6 +1244,61 @@ __global__ void compact_flags_kernel(const uint8_t* __restrict__ flags, int64_t 
     if (threadIdx.x == 0) count[b] = base;
 }
 
+// Row regrouping of the trust fine pass: a few rows have an embedding neighbour
+// far away in input space, so their largest threshold covers most reference tiles, and every
+// 256-row block holding one of them is flagged for most tiles.  The coarse pass records the
+// tiles of every row (rowflags); rows with many tiles are moved behind the others (both groups
+// keep their cluster order), and each new block's tile list is the union of its rows' tiles.
+__global__ void row_tiles_kernel(const uint8_t* __restrict__ rowflags, int64_t rows, int nt, int32_t* __restrict__ cnt)
+{
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= rows) return;
+    int c = 0;
+    for (int t = lane; t < nt; t += 32) c += rowflags[i * nt + t];
+    c = warp_sum(c);
+    if (lane == 0) cnt[i] = c;
+}
+
+__global__ void regroup_keys_kernel(const int32_t* __restrict__ cnt, int64_t rows, int cut, uint32_t* __restrict__ keys,
+                                    int32_t* __restrict__ vals)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    keys[i] = (cnt[i] > cut ? 0x80000000u : 0u) | (uint32_t)i;
+    vals[i] = (int32_t)i;
+}
+
+__global__ void compose_perm_kernel(const int32_t* __restrict__ qperm, const int32_t* __restrict__ pos2, int64_t rows,
+                                    int32_t* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows) out[i] = qperm[pos2[i]];
+}
+
+// flags[b][t] = OR over the rows r' of new block b (256 rows) of rowflags[pos2[r']][t]
+__global__ void block_flags_kernel(const uint8_t* __restrict__ rowflags, const int32_t* __restrict__ pos2, int64_t rows,
+                                   int nt, uint8_t* __restrict__ flags)
+{
+    const int64_t b = blockIdx.x;
+    const int64_t r0 = b * 256, r1 = r0 + 256 < rows ? r0 + 256 : rows;
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        uint8_t f = 0;
+        for (int64_t r = r0; r < r1 && !f; ++r) f = rowflags[(int64_t)pos2[r] * nt + t];
+        flags[b * nt + t] = f;
+    }
+}
+
+// chunk c = (block, offset, length): its own tile list (row c of lists, length <= ch)
+__global__ void chunk_lists_kernel(const int32_t* __restrict__ desc, const int32_t* __restrict__ tl, int nt, int ch,
+                                   int32_t* __restrict__ cblock, int32_t* __restrict__ lists, int32_t* __restrict__ cnt)
+{
+    const int64_t c = blockIdx.x;
+    const int b = desc[3 * c], off = desc[3 * c + 1], len = desc[3 * c + 2];
+    for (int i = threadIdx.x; i < len; i += blockDim.x) lists[c * ch + i] = tl[(int64_t)b * nt + off + i];
+    if (threadIdx.x == 0) { cblock[c] = b; cnt[c] = len; }
+}
+
 __global__ void order_maps_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ pos_of)
 {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1394,8 +1463,9 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     // reference tiles where some row of a 256-row block may reach its largest threshold; the
     // split-precision pass then visits only those tiles (the others are certainly above every
     // threshold of every row of the block and add nothing to any count)
-    Scratch flags, tl, tcnt;
+    Scratch flags, tl, tcnt, rowfl, rcnt, rkeys, pos2, qperm2;
     const int64_t nqb = (qblocks + 1) / 2, ntl = (n + TC_BN - 1) / TC_BN;
+    g_last_regrouped = 0;
     if (ordered && !getenv("UMAP_TC_NO_COARSE")) {
         UMAP_TRY(flags.alloc((size_t)nqb * ntl, s));
         UMAP_CUDA_TRY(cudaMemsetAsync(flags.p, 0, (size_t)nqb * ntl, s));
@@ -1405,6 +1475,12 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         ac.kblocks = d_pad / TC_BK;   // hi part only
         ac.flags = flags.as<uint8_t>();
         ac.tile_ld = (int)ntl;
+        const bool regroup = !getenv("UMAP_TC_NO_REGROUP");  // A/B knob
+        if (regroup) {
+            UMAP_TRY(rowfl.alloc((size_t)rows * ntl, s));
+            UMAP_CUDA_TRY(cudaMemsetAsync(rowfl.p, 0, (size_t)rows * ntl, s));
+            ac.rowflags = rowfl.as<uint8_t>();
+        }
         {
             // single BF16 product with folded norms: representation (2 * 2^-8 + 2^-16) S / 2,
             // accumulation of d_pad products onto partial sums up to S, R2's own error, norms
@@ -1415,6 +1491,48 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         }
         if (const char* mg = unsafe_env("UMAP_TC_COARSE_MARGIN")) ac.margin = (float)atof(mg);  // measurement only
         UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
+        if (regroup) {
+            // rows whose own tile count exceeds twice the median go behind the others
+            UMAP_TRY(rcnt.alloc(sizeof(int32_t) * (size_t)rows, s));
+            row_tiles_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(rowfl.as<uint8_t>(), rows, (int)ntl, rcnt.as<int32_t>());
+            UMAP_LAUNCH_CHECK("row_tiles_kernel");
+            std::vector<int32_t> hc((size_t)rows);
+            UMAP_CUDA_TRY(cudaMemcpyAsync(hc.data(), rcnt.p, sizeof(int32_t) * (size_t)rows, cudaMemcpyDeviceToHost, s));
+            UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+            std::vector<int32_t> sorted_c = hc;
+            std::nth_element(sorted_c.begin(), sorted_c.begin() + rows / 2, sorted_c.end());
+            const int cut = std::max(8, 2 * sorted_c[(size_t)(rows / 2)]);
+            int64_t n_out = 0;
+            for (int32_t c : hc) n_out += c > cut;
+            g_last_regrouped = n_out;
+            if (n_out > 0) {
+                UMAP_TRY(rkeys.alloc(sizeof(uint32_t) * (size_t)rows, s));
+                UMAP_TRY(pos2.alloc(sizeof(int32_t) * (size_t)rows, s));
+                UMAP_TRY(qperm2.alloc(sizeof(int32_t) * (size_t)rows, s));
+                regroup_keys_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(rcnt.as<int32_t>(), rows, cut,
+                                                                       rkeys.as<uint32_t>(), pos2.as<int32_t>());
+                UMAP_LAUNCH_CHECK("regroup_keys_kernel");
+                UMAP_TRY(sort_pairs_u32(rkeys.as<uint32_t>(), pos2.as<int32_t>(), rows, s));
+                compose_perm_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qperm.as<int32_t>(), pos2.as<int32_t>(), rows,
+                                                                       qperm2.as<int32_t>());
+                UMAP_LAUNCH_CHECK("compose_perm_kernel");
+                UMAP_CUDA_TRY(cudaMemcpyAsync(qperm.p, qperm2.p, sizeof(int32_t) * (size_t)rows,
+                                              cudaMemcpyDeviceToDevice, s));
+                // queries, their thresholds and self columns in the new row order
+                shard_order_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qperm.as<int32_t>(), rows, row_begin,
+                                                                       pos_of.as<int32_t>(), k, thr_d2, thr_id,
+                                                                       qrow.as<int32_t>(), selfc.as<int32_t>(),
+                                                                       thr_p.as<float>(), thri_p.as<int32_t>());
+                UMAP_LAUNCH_CHECK("shard_order_kernel");
+                split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X, rows, d, d_pad, colsum.as<double>(),
+                                                                         1.0 / (double)n, xq.as<__nv_bfloat16>(),
+                                                                         qn.as<float>(), qrow.as<int32_t>(), 1);
+                UMAP_LAUNCH_CHECK("split_bf16_kernel");
+                block_flags_kernel<<<(unsigned)nqb, 256, 0, s>>>(rowfl.as<uint8_t>(), pos2.as<int32_t>(), rows,
+                                                                 (int)ntl, flags.as<uint8_t>());
+                UMAP_LAUNCH_CHECK("block_flags_kernel");
+            }
+        }
         int grp = 1;
         if (const char* g = getenv("UMAP_TC_LIST_GROUP")) grp = std::max(1, atoi(g));  // tuning knob
         int rot = 0;
@@ -1425,10 +1543,43 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         a.tile_list = tl.as<int32_t>();
         a.tile_count = tcnt.as<int32_t>();
         a.tile_ld = (int)ntl;
-        std::vector<int32_t> cn((size_t)nqb);  // kept-tile diagnostic (read after the fine pass)
-        UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
+        // chunk the tile lists: a CTA pair walks at most CH tiles, so the block of regrouped rows
+        // (most tiles) is spread over several pairs instead of being the launch's long pole
+        std::vector<int32_t> cn((size_t)nqb);
         UMAP_CUDA_TRY(cudaMemcpyAsync(cn.data(), tcnt.p, sizeof(int32_t) * nqb, cudaMemcpyDeviceToHost, s));
         UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        int CH = 32;
+        if (const char* e = getenv("UMAP_TC_CHUNK")) CH = std::max(1, atoi(e));  // tuning knob
+        int maxc = 0;
+        for (int32_t x : cn) maxc = std::max(maxc, (int)x);
+        Scratch cdesc, cblock, ctl, ccnt;
+        int64_t nchunks = qblocks / 2 + (qblocks & 1);
+        if (maxc > CH) {
+            std::vector<int32_t> desc;  // (block, offset, length) per chunk
+            for (int64_t b = 0; b < nqb; ++b) {
+                const int c = cn[(size_t)b];
+                for (int o = 0; o < std::max(1, c); o += CH) {
+                    desc.push_back((int32_t)b); desc.push_back(o); desc.push_back(std::min(CH, c - o));
+                }
+            }
+            nchunks = (int64_t)desc.size() / 3;
+            UMAP_TRY(cdesc.alloc(sizeof(int32_t) * desc.size(), s));
+            UMAP_TRY(cblock.alloc(sizeof(int32_t) * (size_t)nchunks, s));
+            UMAP_TRY(ctl.alloc(sizeof(int32_t) * (size_t)nchunks * CH, s));
+            UMAP_TRY(ccnt.alloc(sizeof(int32_t) * (size_t)nchunks, s));
+            UMAP_CUDA_TRY(cudaMemcpyAsync(cdesc.p, desc.data(), sizeof(int32_t) * desc.size(), cudaMemcpyHostToDevice, s));
+            chunk_lists_kernel<<<(unsigned)nchunks, 64, 0, s>>>(cdesc.as<int32_t>(), tl.as<int32_t>(), (int)ntl, CH,
+                                                               cblock.as<int32_t>(), ctl.as<int32_t>(), ccnt.as<int32_t>());
+            UMAP_LAUNCH_CHECK("chunk_lists_kernel");
+            a.chunk_block = cblock.as<int32_t>();
+            a.tile_list = ctl.as<int32_t>();
+            a.tile_count = ccnt.as<int32_t>();
+            a.tile_ld = CH;
+            // chunks of one block add into the same rows
+            UMAP_CUDA_TRY(cudaMemsetAsync(hist_use, 0, sizeof(int32_t) * (size_t)rows * k, s));
+            UMAP_CUDA_TRY(cudaMemsetAsync(ambc.p, 0, sizeof(int) * (size_t)rows * NL, s));
+        }
+        UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)(a.chunk_block ? 2 * nchunks : qblocks), 1), s)));
         double m = 0;
         for (int32_t x : cn) m += x;
         g_last_fine_fraction = m / ((double)nqb * (double)ntl);
@@ -1479,6 +1630,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
 }
 
 int64_t last_rank_ambiguous() { return g_last_rank_ambiguous; }
+int64_t last_regrouped_rows() { return g_last_regrouped; }
 double last_fine_fraction() { return g_last_fine_fraction; }
 
 }  // namespace umapb200
