@@ -59,7 +59,8 @@ static const char* const k_prof_names[PROF_NSLOTS] = {
     "knn_tc_kernel (kNN candidates)", "rerank_kernel", "knn_tc_kernel (trust ranks)", "rank_fix_kernel",
     "thresholds_warp_kernel", "grid_knn_kernel", "smooth_knn_kernel", "fuzzy union (5 kernels)",
     "sgd_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
-    "transform_sgd_kernel", "knn_tc_kernel (trust coarse)", "spectral init (3 kernels x iterations)"};
+    "transform_sgd_kernel", "knn_tc_kernel (trust coarse)", "spectral init (3 kernels x iterations)",
+    "trust projection (basis + operands)", "trust regroup + chunking"};
 void count_launch(int n) { g_launches += n; }
 
 umap_status cuda_status(cudaError_t e, const char* what)

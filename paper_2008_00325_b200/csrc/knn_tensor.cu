@@ -34,6 +34,7 @@ namespace umapb200 {
 
 static thread_local int64_t g_last_rank_ambiguous = 0;
 static thread_local int64_t g_last_regrouped = 0;
+static thread_local bool g_last_projected = false;
 static thread_local double g_last_fine_fraction = 1.0;
 
 umap_status topk_merge(const int32_t* idx_in, const float* d2_in, int n_parts, int64_t n, int k_in, int k_out,
@@ -246,6 +247,15 @@ struct TcArgs {
     uint8_t* flags;           // MODE 2 (coarse pass): flags[b * tile_ld + t] = 1 if tile t may matter
     uint8_t* rowflags;        // MODE 2, optional: rowflags[q * tile_ld + t] = 1 if tile t may matter for row q
     const int32_t* chunk_block;  // MODE 1, optional: query block of tile-list chunk c (hist / amb_count added atomically)
+    // MODE 2 on projected operands: per-row slacks (query / reference order) and
+    // the basis bound sigma_max(P); qnorm / rnorm are then the projected norms |z~|^2
+    const float* proj_bq;
+    const float* proj_br;
+    const float* proj_sigma;  // device: bound on sigma_max(P) (+inf if the basis failed: nothing skipped)
+    // MODE 2, optional: per 32-column chunk maxima of rnorm and proj_br (one broadcast load per chunk
+    // instead of a per-lane load and a warp reduction)
+    const float* chunk_rmax;
+    const float* chunk_bmax;
 };
 
 constexpr int TC_KT = 16;   // max thresholds per row in RANK mode
@@ -555,6 +565,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const bool valid = q < a.nq;
         const float qn = valid ? a.qnorm[q] : 0.0f;
         const float tmax = valid ? a.thr_d2[q * a.k + (a.k - 1)] : -INFINITY;
+        // projected operands: skip only if |z~_q - z~_r| - E-slack - b_q - b_r > sigma sqrt(tmax / r_lo)
+        // (then |x_q - x_r| > sqrt(tmax / r_lo) and R2 >= d2 r_lo > tmax); kept iff
+        // d2~_P <= (A_q + b_q + b_r)^2 + E
+        const bool proj = a.proj_bq != nullptr;
+        const float aq = (proj && valid) ? *a.proj_sigma * sqrtf(tmax / a.r_lo) * 1.000001f + a.proj_bq[q] : 0.0f;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
@@ -569,11 +584,28 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
                 const int valid_cols = (int)imin64(32, r_hi - jb);
-                const float rn_l = lane < valid_cols ? __ldg(a.rnorm + jb + lane) : 0.0f;
-                float rmax = rn_l;
+                float rmax;
+                if (a.chunk_rmax) {
+                    rmax = __ldg(a.chunk_rmax + (jb >> 5));
+                } else {
+                    rmax = lane < valid_cols ? __ldg(a.rnorm + jb + lane) : 0.0f;
 #pragma unroll
-                for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-                const float vlim = -0.5f * (tmax + a.margin * (qn + rmax));
+                    for (int o = 16; o; o >>= 1) rmax = fmaxf(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                }
+                float lim = tmax;
+                if (proj) {
+                    float br;
+                    if (a.chunk_bmax) {
+                        br = __ldg(a.chunk_bmax + (jb >> 5));
+                    } else {
+                        br = lane < valid_cols ? __ldg(a.proj_br + jb + lane) : 0.0f;
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) br = fmaxf(br, __shfl_xor_sync(0xffffffffu, br, o));
+                    }
+                    const float s = aq + br;
+                    lim = s * s * 1.000001f;
+                }
+                const float vlim = -0.5f * (lim + a.margin * (qn + rmax));
                 uint32_t cm = 0;
 #pragma unroll
                 for (int u = 0; u < 32; ++u) cm |= (uint32_t)(v[u] >= vlim) << u;
@@ -795,6 +827,103 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     if (lane == 0) norms[row] = acc;
     __syncwarp();
     write_norm_extras(Xc + row * d_pad, d_pad, acc, role, lane);
+}
+
+// Projected coarse pass: Z = X_c P (n x KP fp32, original row order), X_c = fl(x -
+// mean) as in split_bf16_kernel, P the d x KP basis of pca_basis.  64 rows x KP columns per CTA,
+// 256 threads with 8 x (KP / 32) outputs each, d staged in slabs of 16.
+template <int KP>
+__global__ void __launch_bounds__(256) proj_gemm_kernel(const float* __restrict__ X, int64_t n, int d,
+                                                        const double* __restrict__ colsum, double inv_n,
+                                                        const float* __restrict__ P, float* __restrict__ Z)
+{
+    constexpr int CPT = KP / 32;  // columns per thread (tc + 32 j)
+    __shared__ float As[16][64 + 1], Bs[16][KP];
+    const int tid = threadIdx.x;
+    const int tr = tid >> 5, tc = tid & 31;  // rows tr * 8 .. tr * 8 + 7
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    float acc[8][CPT];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) acc[i][j] = 0.0f;
+    for (int f0 = 0; f0 < d; f0 += 16) {
+        for (int i = tid; i < 64 * 16; i += 256) {
+            const int rr = i >> 4, ff = i & 15;
+            const int64_t row = r0 + rr;
+            const int f = f0 + ff;
+            As[ff][rr] = (row < n && f < d) ? X[row * d + f] - (float)(colsum[f] * inv_n) : 0.0f;
+        }
+        for (int i = tid; i < 16 * KP; i += 256) {
+            const int ff = i / KP, c = i % KP;
+            Bs[ff][c] = (f0 + ff < d) ? P[(int64_t)(f0 + ff) * KP + c] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ff = 0; ff < 16; ++ff) {
+            float a[8], b[CPT];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = As[ff][tr * 8 + i];
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) b[j] = Bs[ff][tc + 32 * j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = r0 + tr * 8 + i;
+        if (row < n)
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) Z[row * KP + tc + 32 * j] = acc[i][j];
+    }
+}
+
+// out[c] = max of v[32 c .. 32 c + 31] (v >= 0; a missing tail counts as 0)
+__global__ void chunk_max_kernel(const float* __restrict__ v, int64_t n, float* __restrict__ out)
+{
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (c * 32 >= n) return;
+    float m = c * 32 + lane < n ? v[c * 32 + lane] : 0.0f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) out[c] = m;
+}
+
+// Projected operand rows in a given order (rowmap: output row -> input row): BF16 z (K columns),
+// zeros up to d_pad - 6, the folded norms (role 1 / 2) of zn = |z~|^2 (fp32 of the fp32 z~); and
+// the per-row slack bvec = sigma (1.01 u |x_c|) + sqrt(K) gamma_d sigma |x_c| covering the
+// centring rounding and the fp32 projection error (|x_c|^2 = xnorm, the split operands' norms).
+__global__ void proj_operand_kernel(const float* __restrict__ Z, int KP, int K, int64_t rows, int d_pad,
+                                    const int32_t* __restrict__ rowmap, const float* __restrict__ xnorm,
+                                    const float* __restrict__ sigma_p, float gamma_d, int role, __nv_bfloat16* __restrict__ Zb, float* __restrict__ zn,
+                                    float* __restrict__ bvec)
+{
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const int64_t src = rowmap ? (int64_t)rowmap[row] : row;
+    __nv_bfloat16* o = Zb + row * (int64_t)d_pad;
+    float acc = 0.0f;
+    for (int c = lane; c < d_pad - 6; c += 32) {
+        const float z = c < K ? Z[src * KP + c] : 0.0f;
+        acc = fmaf(z, z, acc);
+        o[c] = __float2bfloat16_rn(z);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        zn[row] = acc;
+        const float sigma = *sigma_p;
+        const float xn = sqrtf(xnorm[row]) * 1.0001f;
+        const float u = 5.9604645e-8f;
+        bvec[row] = (sigma * 1.01f * u * xn + sqrtf((float)K) * gamma_d * sigma * xn) * 1.01f;
+    }
+    __syncwarp();
+    write_norm_extras(o, d_pad, acc, role, lane);
 }
 
 // split-BF16 operands for the RANK mode: x_c = x - mean (fp32), hi = bf16(x_c),
@@ -1345,6 +1474,8 @@ __global__ void unscatter_hist_kernel(const int32_t* __restrict__ qperm, int64_t
 
 umap_status cluster_order(const float* Y, int64_t n, int d_emb, int32_t* perm, cudaStream_t s);
 umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_t s);
+umap_status pca_basis(const float* X, int64_t n, int d, const double* colsum, int K, float* P, float* sigma,
+                      cudaStream_t s);
 
 // Input-space rank counts of trustworthiness with the tensor-core GEMM (R16): queries =
 // rows [row_begin, row_end) of X, references = all of X.  Exact thresholds in, exact
@@ -1490,8 +1621,76 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             ac.margin = (float)(1.1 * c);
         }
         if (const char* mg = unsafe_env("UMAP_TC_COARSE_MARGIN")) ac.margin = (float)atof(mg);  // measurement only
-        UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
+        // projected coarse pass (d >= 256): the same test on z = P^T x_c, K = 122 principal
+        // directions (+ 6 folded-norm columns = 2 K slabs instead of d_pad / 64), with the slack of
+        // every rounding step in the per-row bound; any failure of the basis keeps
+        // the full-dimensional pass
+        constexpr int KPJ = 122, KPG = 128, DPZ = 128;
+        Scratch pbk, pbp, zf, zq, zr, znq, znr, pbq, pbr, cmr, cmb, psig;
+        CUtensorMap map_zq, map_zr;
+        bool projected = false;
+        if (d >= 256 && !getenv("UMAP_TC_NO_PROJ")) {
+            ProfScope ps_proj(PROF_TRUST_PROJ, s);
+            UMAP_TRY(pbk.alloc(sizeof(float) * (size_t)d * KPJ, s));
+            UMAP_TRY(psig.alloc(sizeof(float), s));
+            const float* sigma = psig.as<float>();
+            if (pca_basis(X, n, d, colsum.as<double>(), KPJ, pbk.as<float>(), psig.as<float>(), s) == UMAP_OK) {
+                UMAP_TRY(pbp.alloc(sizeof(float) * (size_t)d * KPG, s));
+                UMAP_CUDA_TRY(cudaMemsetAsync(pbp.p, 0, sizeof(float) * (size_t)d * KPG, s));
+                UMAP_CUDA_TRY(cudaMemcpy2DAsync(pbp.p, sizeof(float) * KPG, pbk.p, sizeof(float) * KPJ,
+                                                sizeof(float) * KPJ, (size_t)d, cudaMemcpyDeviceToDevice, s));
+                UMAP_TRY(zf.alloc(sizeof(float) * (size_t)n * KPG, s));
+                proj_gemm_kernel<KPG><<<(unsigned)ceil_div(n, 64), 256, 0, s>>>(X, n, d, colsum.as<double>(),
+                                                                                1.0 / (double)n, pbp.as<float>(),
+                                                                                zf.as<float>());
+                UMAP_LAUNCH_CHECK("proj_gemm_kernel");
+                const double u = std::ldexp(1.0, -24);
+                const float gamma_d = (float)(d * u / (1.0 - d * u));
+                UMAP_TRY(zq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * DPZ, s));
+                UMAP_TRY(znq.alloc(sizeof(float) * (size_t)rows, s));
+                UMAP_TRY(pbq.alloc(sizeof(float) * (size_t)rows, s));
+                proj_operand_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(
+                    zf.as<float>(), KPG, KPJ, rows, DPZ, qrow.as<int32_t>(), qn.as<float>(), sigma, gamma_d, 1,
+                    zq.as<__nv_bfloat16>(), znq.as<float>(), pbq.as<float>());
+                UMAP_LAUNCH_CHECK("proj_operand_kernel");
+                UMAP_TRY(zr.alloc(sizeof(__nv_bfloat16) * (size_t)n * DPZ, s));
+                UMAP_TRY(znr.alloc(sizeof(float) * (size_t)n, s));
+                UMAP_TRY(pbr.alloc(sizeof(float) * (size_t)n, s));
+                proj_operand_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(
+                    zf.as<float>(), KPG, KPJ, n, DPZ, perm.as<int32_t>(), rn.as<float>(), sigma, gamma_d, 2,
+                    zr.as<__nv_bfloat16>(), znr.as<float>(), pbr.as<float>());
+                UMAP_LAUNCH_CHECK("proj_operand_kernel");
+                UMAP_TRY(make_map(&map_zq, zq.as<__nv_bfloat16>(), rows, DPZ, TC_BM));
+                UMAP_TRY(make_map(&map_zr, zr.as<__nv_bfloat16>(), n, DPZ, TC_BN / tc_cg()));
+                ac.kblocks = DPZ / TC_BK;
+                ac.qnorm = znq.as<float>();
+                ac.rnorm = znr.as<float>();
+                ac.proj_bq = pbq.as<float>();
+                ac.proj_br = pbr.as<float>();
+                ac.proj_sigma = sigma;
+                UMAP_TRY(cmr.alloc(sizeof(float) * (size_t)(n / 32 + 1), s));
+                UMAP_TRY(cmb.alloc(sizeof(float) * (size_t)(n / 32 + 1), s));
+                chunk_max_kernel<<<(unsigned)ceil_div(n / 32 + 1, 8), 256, 0, s>>>(znr.as<float>(), n, cmr.as<float>());
+                UMAP_LAUNCH_CHECK("chunk_max_kernel");
+                chunk_max_kernel<<<(unsigned)ceil_div(n / 32 + 1, 8), 256, 0, s>>>(pbr.as<float>(), n, cmb.as<float>());
+                UMAP_LAUNCH_CHECK("chunk_max_kernel");
+                ac.chunk_rmax = cmr.as<float>();
+                ac.chunk_bmax = cmb.as<float>();
+                // BF16 representation + accumulation of DPZ products + norms + final ops (no R2 term:
+                // R2 enters through tmax / r_lo), times 1.1
+                ac.margin = (float)(1.1 * ((2.0 * std::ldexp(1.0, -8) + std::ldexp(1.0, -16)) * 0.5 + DPZ * 2.0 * u +
+                                           ((KPJ + 31) / 32 + 5) * u + 3.0 * u));
+                projected = true;
+            }
+        }
+        g_last_projected = projected;
+        if (projected) {
+            UMAP_TRY((launch_tc<32, 2>(map_zq, map_zr, ac, dim3((unsigned)qblocks, 1), s)));
+        } else {
+            UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
+        }
         if (regroup) {
+            ProfScope ps_rg(PROF_TRUST_REGROUP, s);
             // rows whose own tile count exceeds twice the median go behind the others
             UMAP_TRY(rcnt.alloc(sizeof(int32_t) * (size_t)rows, s));
             row_tiles_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(rowfl.as<uint8_t>(), rows, (int)ntl, rcnt.as<int32_t>());
