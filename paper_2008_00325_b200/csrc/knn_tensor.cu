@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "bulk.cuh"
+#include "gemm.cuh"
 
 namespace umapb200 {
 
@@ -829,59 +830,6 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     write_norm_extras(Xc + row * d_pad, d_pad, acc, role, lane);
 }
 
-// Projected coarse pass: Z = X_c P (n x KP fp32, original row order), X_c = fl(x -
-// mean) as in split_bf16_kernel, P the d x KP basis of pca_basis.  64 rows x KP columns per CTA,
-// 256 threads with 8 x (KP / 32) outputs each, d staged in slabs of 16.
-template <int KP>
-__global__ void __launch_bounds__(256) proj_gemm_kernel(const float* __restrict__ X, int64_t n, int d,
-                                                        const double* __restrict__ colsum, double inv_n,
-                                                        const float* __restrict__ P, float* __restrict__ Z)
-{
-    constexpr int CPT = KP / 32;  // columns per thread (tc + 32 j)
-    __shared__ float As[16][64 + 1], Bs[16][KP];
-    const int tid = threadIdx.x;
-    const int tr = tid >> 5, tc = tid & 31;  // rows tr * 8 .. tr * 8 + 7
-    const int64_t r0 = (int64_t)blockIdx.x * 64;
-    float acc[8][CPT];
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < CPT; ++j) acc[i][j] = 0.0f;
-    for (int f0 = 0; f0 < d; f0 += 16) {
-        for (int i = tid; i < 64 * 16; i += 256) {
-            const int rr = i >> 4, ff = i & 15;
-            const int64_t row = r0 + rr;
-            const int f = f0 + ff;
-            As[ff][rr] = (row < n && f < d) ? X[row * d + f] - (float)(colsum[f] * inv_n) : 0.0f;
-        }
-        for (int i = tid; i < 16 * KP; i += 256) {
-            const int ff = i / KP, c = i % KP;
-            Bs[ff][c] = (f0 + ff < d) ? P[(int64_t)(f0 + ff) * KP + c] : 0.0f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int ff = 0; ff < 16; ++ff) {
-            float a[8], b[CPT];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = As[ff][tr * 8 + i];
-#pragma unroll
-            for (int j = 0; j < CPT; ++j) b[j] = Bs[ff][tc + 32 * j];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                for (int j = 0; j < CPT; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t row = r0 + tr * 8 + i;
-        if (row < n)
-#pragma unroll
-            for (int j = 0; j < CPT; ++j) Z[row * KP + tc + 32 * j] = acc[i][j];
-    }
-}
-
 // out[c] = max of v[32 c .. 32 c + 31] (v >= 0; a missing tail counts as 0)
 __global__ void chunk_max_kernel(const float* __restrict__ v, int64_t n, float* __restrict__ out)
 {
@@ -1625,25 +1573,26 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         // directions (+ 6 folded-norm columns = 2 K slabs instead of d_pad / 64), with the slack of
         // every rounding step in the per-row bound; any failure of the basis keeps
         // the full-dimensional pass
-        constexpr int KPJ = 122, KPG = 128, DPZ = 128;
-        Scratch pbk, pbp, zf, zq, zr, znq, znr, pbq, pbr, cmr, cmb, psig;
+        constexpr int KPG = 128;
+        int KPJ = 122, DPZ = 128;  // projected dimensions (+ 6 folded-norm columns = DPZ)
+        if (const char* e = getenv("UMAP_TC_PROJ_K")) {  // tuning knob: 58 (one K slab) or 122 (two)
+            KPJ = atoi(e) <= 58 ? 58 : 122;
+            DPZ = KPJ + 6;
+        }
+        Scratch pbp, zf, zq, zr, znq, znr, pbq, pbr, cmr, cmb, psig;
         CUtensorMap map_zq, map_zr;
         bool projected = false;
         if (d >= 256 && !getenv("UMAP_TC_NO_PROJ")) {
             ProfScope ps_proj(PROF_TRUST_PROJ, s);
-            UMAP_TRY(pbk.alloc(sizeof(float) * (size_t)d * KPJ, s));
+            UMAP_TRY(pbp.alloc(sizeof(float) * (size_t)d * KPG, s));
             UMAP_TRY(psig.alloc(sizeof(float), s));
             const float* sigma = psig.as<float>();
-            if (pca_basis(X, n, d, colsum.as<double>(), KPJ, pbk.as<float>(), psig.as<float>(), s) == UMAP_OK) {
-                UMAP_TRY(pbp.alloc(sizeof(float) * (size_t)d * KPG, s));
-                UMAP_CUDA_TRY(cudaMemsetAsync(pbp.p, 0, sizeof(float) * (size_t)d * KPG, s));
-                UMAP_CUDA_TRY(cudaMemcpy2DAsync(pbp.p, sizeof(float) * KPG, pbk.p, sizeof(float) * KPJ,
-                                                sizeof(float) * KPJ, (size_t)d, cudaMemcpyDeviceToDevice, s));
+            if (pca_basis(X, n, d, colsum.as<double>(), KPJ, pbp.as<float>(), psig.as<float>(), s) == UMAP_OK) {
                 UMAP_TRY(zf.alloc(sizeof(float) * (size_t)n * KPG, s));
-                proj_gemm_kernel<KPG><<<(unsigned)ceil_div(n, 64), 256, 0, s>>>(X, n, d, colsum.as<double>(),
-                                                                                1.0 / (double)n, pbp.as<float>(),
-                                                                                zf.as<float>());
-                UMAP_LAUNCH_CHECK("proj_gemm_kernel");
+                tgemm128_kernel<false><<<(unsigned)ceil_div(n, 128), 256, 0, s>>>(X, n, 1, d, d, colsum.as<double>(),
+                                                                                 1.0 / (double)n, pbp.as<float>(),
+                                                                                 zf.as<float>());
+                UMAP_LAUNCH_CHECK("tgemm128_kernel");
                 const double u = std::ldexp(1.0, -24);
                 const float gamma_d = (float)(d * u / (1.0 - d * u));
                 UMAP_TRY(zq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * DPZ, s));
