@@ -4,7 +4,7 @@
 TAG=${1:-r01}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_${TAG}.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/pytest_gpu_${TAG}.log
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -30 > gpurun_out/pytest_gpu_${TAG}.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 600 python bench.py --sgd-mode hogwild --no-cpu-baseline --no-e2e > gpurun_out/bench_hog_${TAG}.json 2>> gpurun_out/bench_${TAG}.err
@@ -16,6 +16,8 @@ ncu -i /tmp/prof_${TAG}.ncu-rep --page raw --csv --print-units base > gpurun_out
 ncu -i /tmp/prof_${TAG}.ncu-rep --page details > gpurun_out/prof_${TAG}_details.txt 2>/dev/null
 ncu -i /tmp/prof_${TAG}.ncu-rep --page source --csv --print-source sass -k regex:knn_tc --launch-skip 2 --launch-count 1 > gpurun_out/prof_${TAG}_trust_sass.csv 2>/dev/null
 ncu -i /tmp/prof_${TAG}.ncu-rep --page source --csv --print-source sass -k regex:sgd_ > gpurun_out/prof_${TAG}_sgd_sass.csv 2>/dev/null
+python tools/ncu_summary.py gpurun_out/prof_${TAG}_raw.csv gpurun_out/ncu_${TAG}.json > gpurun_out/ncu_${TAG}_summary.txt 2>&1
+python tools/launches.py gpurun_out/launches_${TAG}.csv > gpurun_out/launches_${TAG}.txt 2>&1
 gzip -f gpurun_out/prof_${TAG}_*sass.csv gpurun_out/prof_${TAG}_raw.csv
 du -sh gpurun_out
 ls -la gpurun_out
