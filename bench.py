@@ -496,7 +496,7 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------------------------- scaling legs
-def scaling_legs(args, world, rank, warmup=1, steps=2):
+def scaling_legs(args, world, rank, warmup=2, steps=3):
     """The two BASELINE.json configs that the paper scales across GPUs (App. B P:343,
     P:480-485), timed at every N (weak in the index rows per rank for C4, partitioned for C5):
 

@@ -9,7 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 timeout 600 python bench.py --sgd-mode hogwild --no-cpu-baseline --no-e2e > gpurun_out/bench_hog_${TAG}.json 2>> gpurun_out/bench_${TAG}.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/launches_${TAG}.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-scaling-legs > gpurun_out/launches_${TAG}.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'knn_tc|sgd_|rerank|rank_fix' \
     -c 6 -o /tmp/prof_${TAG} -f python tools/profile_step.py --knn-mode tensor > gpurun_out/prof_${TAG}.log 2>&1
 ncu -i /tmp/prof_${TAG}.ncu-rep --page raw --csv --print-units base > gpurun_out/prof_${TAG}_raw.csv 2>/dev/null
