@@ -248,6 +248,7 @@ struct TcArgs {
     uint8_t* flags;           // MODE 2 (coarse pass): flags[b * tile_ld + t] = 1 if tile t may matter
     uint8_t* rowflags;        // MODE 2, optional: rowflags[q * tile_ld + t] = 1 if tile t may matter for row q
     const int32_t* chunk_block;  // MODE 1, optional: query block of tile-list chunk c (hist / amb_count added atomically)
+    int rotate;               // MODE 0 without tile lists: start at the pair's proportional tile and wrap
     // MODE 2 on projected operands: per-row slacks (query / reference order) and
     // the basis bound sigma_max(P); qnorm / rnorm are then the projected norms |z~|^2
     const float* proj_bq;
@@ -310,6 +311,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     const int pblk = (int)(blockIdx.x >> 1);  // 256-row query block of this CTA (both CTAs of a pair)
     const int ntiles = a.tile_count ? a.tile_count[pblk] : ntiles_all;
     const int32_t* tlist = a.tile_count ? a.tile_list + (int64_t)pblk * a.tile_ld : nullptr;
+    // rotate (no tile list): the pair starts at the reference tile proportional to its query rows
+    // (in pivot order: its own neighbourhood) and wraps around; the same for both CTAs of a pair
+    const int rot0 = (a.rotate && !tlist && ntiles_all > 0)
+                         ? (int)(((int64_t)pblk * 2 * TC_BM * ntiles_all / (a.nq > 0 ? a.nq : 1)) % ntiles_all) : 0;
+    auto tile_at = [&](int t) { return tlist ? tlist[t] : (rot0 ? (t + rot0) % ntiles_all : t); };
     const int KB = a.kblocks;
 
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
@@ -360,7 +366,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
-                const int y_r = (int)(r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN);
+                const int y_r = (int)(r_lo + (int64_t)tile_at(t) * TC_BN);
                 for (int kb = 0; kb < KB; ++kb) {
 #pragma unroll
                     for (int part = 0; part < PARTS; ++part, ++g) {
@@ -465,7 +471,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
-            const int64_t rb = r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN;
+            const int64_t rb = r_lo + (int64_t)tile_at(t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
             for (int c = half * CP; c < (half + 1) * CP && !(a.debug & 1); c += 32) {
@@ -575,7 +581,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
-            const int tile = tlist ? tlist[t] : t;
+            const int tile = tile_at(t);
             const int64_t rb = r_lo + (int64_t)tile * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
             bool hit = false;
@@ -637,7 +643,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const int64_t q = q0 + row;
         const bool valid = q < a.nq;
         const float qn = valid ? a.qnorm[q] : 0.0f;
-        const int64_t self_j = (valid && a.exclude_self) ? q + a.self_shift : -1;
+        const int64_t self_j =
+            (valid && a.exclude_self) ? (a.self_col ? (int64_t)a.self_col[q] : q + a.self_shift) : -1;
         float kd[KC];
         int32_t ki[KC];
 #pragma unroll
@@ -647,7 +654,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
-            const int64_t rb = r_lo + (int64_t)(tlist ? tlist[t] : t) * TC_BN;
+            const int64_t rb = r_lo + (int64_t)tile_at(t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
 #pragma unroll 1
             for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
@@ -808,11 +815,12 @@ __device__ __forceinline__ void write_norm_extras(__nv_bfloat16* rowp, int d_pad
 // q.r - |q|^2/2 - |r|^2/2 = -d2/2 directly (norms folded into the padding of the last K slab).
 __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
                                    const double* __restrict__ colsum, double inv_n, __nv_bfloat16* __restrict__ Xc,
-                                   float* __restrict__ norms, int role)
+                                   float* __restrict__ norms, int role, const int32_t* __restrict__ rowmap)
 {
-    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t orow = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // output row
     const int lane = threadIdx.x & 31;
-    if (row >= n) return;
+    if (orow >= n) return;
+    const int64_t row = rowmap ? (int64_t)rowmap[orow] : orow;  // input row
     float acc = 0.0f;
     for (int f = lane; f < d_pad; f += 32) {
         __nv_bfloat16 h = __float2bfloat16_rn(0.0f);
@@ -822,12 +830,12 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
             const float hv = __bfloat162float(h);
             acc = fmaf(hv, hv, acc);
         }
-        Xc[row * d_pad + f] = h;
+        Xc[orow * d_pad + f] = h;
     }
     acc = warp_sum(acc);
-    if (lane == 0) norms[row] = acc;
+    if (lane == 0) norms[orow] = acc;
     __syncwarp();
-    write_norm_extras(Xc + row * d_pad, d_pad, acc, role, lane);
+    write_norm_extras(Xc + orow * d_pad, d_pad, acc, role, lane);
 }
 
 // out[c] = max of v[32 c .. 32 c + 31] (v >= 0; a missing tail counts as 0)
@@ -1117,12 +1125,53 @@ umap_status make_map(CUtensorMap* m, const __nv_bfloat16* base, int64_t rows, in
 }
 
 // centred BF16 copy + norms of X (rows n) with the given column mean (colsum / n_mean)
+// ---------------------------------------------------------------- kNN pivot order (round 2)
+// Short-K kNN (d_pad <= 256, e.g. C4's d = 50) is bounded by the top-k' epilogue, whose cost is
+// set by how often a column beats a row's running k'-th best.  With queries and references in
+// pivot order (each row next to the rows nearest the same sampled pivot) every query block meets
+// its own neighbourhood early, the running thresholds tighten sooner and fewer columns enter the
+// insertion loop.  The result does not depend on the order.
+
+// rows[i] = X[i * stride] (the pivot sample)
+__global__ void gather_rows_kernel(const float* __restrict__ X, int64_t m, int64_t stride, int d, float* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m * d) return;
+    const int64_t r = i / d;
+    out[i] = X[r * stride * d + (i - r * d)];
+}
+
+// keys[i] = pivot of row i (the first candidate), vals[i] = i
+__global__ void pivot_keys_kernel(const int32_t* __restrict__ piv, int64_t n, uint32_t* __restrict__ keys,
+                                  int32_t* __restrict__ vals)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = (uint32_t)max(piv[i], 0);
+    vals[i] = (int32_t)i;
+}
+
+// candidates of query-operand row i (reference-operand ids) -> the caller's order and ids
+__global__ void unpermute_cand_kernel(const int32_t* __restrict__ ci, const float* __restrict__ cd,
+                                      const int32_t* __restrict__ qperm, const int32_t* __restrict__ rperm, int64_t nq,
+                                      int kc, int64_t index_offset, int32_t* __restrict__ oi, float* __restrict__ od)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq * kc) return;
+    const int64_t row = i / kc;
+    const int t = (int)(i - row * kc);
+    const int32_t c = ci[i];
+    const int64_t o = (int64_t)qperm[row] * kc + t;
+    oi[o] = c >= 0 ? (int32_t)(rperm[c] + index_offset) : -1;
+    od[o] = cd[i];
+}
+
 umap_status prep_bf16(const float* X, int64_t n, int d, int d_pad, const double* colsum, int64_t n_mean,
-                      __nv_bfloat16* Xc, float* norms, int role, cudaStream_t s)
+                      __nv_bfloat16* Xc, float* norms, int role, cudaStream_t s, const int32_t* rowmap = nullptr)
 {
     if (n == 0) return UMAP_OK;
     center_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum, 1.0 / (double)n_mean, Xc, norms,
-                                                             role);
+                                                             role, rowmap);
     UMAP_LAUNCH_CHECK("center_bf16_kernel");
     return UMAP_OK;
 }
@@ -1188,9 +1237,35 @@ umap_status launch_tc(const CUtensorMap& mq, const CUtensorMap& mr, const TcArgs
 
 // Tensor-core candidate kNN + exact re-rank.  Centring uses the column means of the
 // reference set (R3).  kc = candidates per row (k <= kc <= 32).
+static umap_status knn_tensor_impl(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
+                                   int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared,
+                                   int32_t* idx, float* dist, cudaStream_t s, bool order_ok);
+namespace {
+__global__ void order_maps_kernel(const int32_t* __restrict__ perm, int64_t n, int32_t* __restrict__ pos_of);
+}  // namespace
+umap_status sort_pairs_u32(uint32_t* keys, int32_t* vals, int64_t n, cudaStream_t s);
+
 umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
                        int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared, int32_t* idx,
                        float* dist, cudaStream_t s)
+{
+    return knn_tensor_impl(Xq, nq, Xr, nr, d, k, kc, self_shift, exclude_self, index_offset, out_squared, idx, dist, s,
+                           true);
+}
+
+// self-column of query-operand row i in reference-operand order (-1: none)
+__global__ void self_col_kernel(const int32_t* __restrict__ qperm, const int32_t* __restrict__ rpos, int64_t nq,
+                                int64_t nr, int64_t self_shift, int32_t* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nq) return;
+    const int64_t r = (int64_t)qperm[i] + self_shift;
+    out[i] = (r >= 0 && r < nr) ? rpos[r] : -1;
+}
+
+static umap_status knn_tensor_impl(const float* Xq, int64_t nq, const float* Xr, int64_t nr, int d, int k, int kc,
+                                   int64_t self_shift, int exclude_self, int64_t index_offset, int out_squared,
+                                   int32_t* idx, float* dist, cudaStream_t s, bool order_ok)
 {
     if (nq == 0) return UMAP_OK;
     kc = std::min(TC_KCMAX, std::max(kc, 2 * k));
@@ -1211,23 +1286,73 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
         colsum_kernel<<<grid, 256, 0, s>>>(Xr, nr, d, colsum.as<double>());
         UMAP_LAUNCH_CHECK("colsum_kernel");
     }
+    // pivot order for short K (see gather_rows_kernel); off for small problems and the nested
+    // pivot searches
+    const bool self_case = Xq == Xr && nq == nr && self_shift == 0;
+    // (long K, e.g. C2: measured slower, 6.3 -> 7.2 ms with the pivot search; the MMA bounds the tile there)
+    bool pivot_order = order_ok && (d_pad <= 256 || getenv("UMAP_TC_KNN_ORDER_ALL")) && nr >= 64 * (int64_t)TC_BN &&
+                       nq >= 16 * (int64_t)TC_BN && !getenv("UMAP_TC_KNN_NO_ORDER");
+    Scratch rperm, qperm_s, pivots, pidx, pdist, keys, rposs, selfc;
+    const int32_t* qperm = nullptr;
+    if (pivot_order) {
+        ProfScope ps_pr(PROF_KNN_PRUNE, s);
+        const int64_t P = std::min<int64_t>(4096, std::max<int64_t>(16, nr / TC_BN));
+        const int64_t stride = nr / P;
+        UMAP_TRY(pivots.alloc(sizeof(float) * (size_t)P * d, s));
+        gather_rows_kernel<<<(unsigned)ceil_div(P * d, 256), 256, 0, s>>>(Xr, P, stride, d, pivots.as<float>());
+        UMAP_LAUNCH_CHECK("gather_rows_kernel");
+        const int64_t nmax = std::max(nq, nr);
+        UMAP_TRY(pidx.alloc(sizeof(int32_t) * (size_t)nmax, s));
+        UMAP_TRY(pdist.alloc(sizeof(float) * (size_t)nmax, s));
+        UMAP_TRY(keys.alloc(sizeof(uint32_t) * (size_t)nmax, s));
+        auto order = [&](const float* Xs, int64_t ns, Scratch& perm) -> umap_status {
+            // nearest pivot (BF16 candidates + exact re-rank, k = 1), then rows sorted by pivot
+            UMAP_TRY(knn_tensor_impl(Xs, ns, pivots.as<float>(), P, d, 1, 2, 0, 0, 0, 1, pidx.as<int32_t>(),
+                                     pdist.as<float>(), s, false));
+            UMAP_TRY(perm.alloc(sizeof(int32_t) * (size_t)ns, s));
+            pivot_keys_kernel<<<ceil_div(ns, 256), 256, 0, s>>>(pidx.as<int32_t>(), ns, keys.as<uint32_t>(),
+                                                               perm.as<int32_t>());
+            UMAP_LAUNCH_CHECK("pivot_keys_kernel");
+            return sort_pairs_u32(keys.as<uint32_t>(), perm.as<int32_t>(), ns, s);
+        };
+        UMAP_TRY(order(Xr, nr, rperm));
+        if (self_case) {
+            qperm = rperm.as<int32_t>();
+        } else {
+            UMAP_TRY(order(Xq, nq, qperm_s));
+            qperm = qperm_s.as<int32_t>();
+        }
+        if (exclude_self && !self_case) {
+            UMAP_TRY(rposs.alloc(sizeof(int32_t) * (size_t)nr, s));
+            order_maps_kernel<<<ceil_div(nr, 256), 256, 0, s>>>(rperm.as<int32_t>(), nr, rposs.as<int32_t>());
+            UMAP_LAUNCH_CHECK("order_maps_kernel");
+            UMAP_TRY(selfc.alloc(sizeof(int32_t) * (size_t)nq, s));
+            self_col_kernel<<<ceil_div(nq, 256), 256, 0, s>>>(qperm, rposs.as<int32_t>(), nq, nr, self_shift,
+                                                              selfc.as<int32_t>());
+            UMAP_LAUNCH_CHECK("self_col_kernel");
+        }
+    }
     UMAP_TRY(xr16.alloc(sizeof(__nv_bfloat16) * (size_t)nr * d_pad, s));
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)nr, s));
-    UMAP_TRY(prep_bf16(Xr, nr, d, d_pad, colsum.as<double>(), nr, xr16.as<__nv_bfloat16>(), rn.as<float>(), 2, s));
+    UMAP_TRY(prep_bf16(Xr, nr, d, d_pad, colsum.as<double>(), nr, xr16.as<__nv_bfloat16>(), rn.as<float>(), 2, s,
+                       pivot_order ? rperm.as<int32_t>() : nullptr));
     // queries always get their own copy (A role; for a self-kNN the same rows in the other role)
     UMAP_TRY(xq16.alloc(sizeof(__nv_bfloat16) * (size_t)nq * d_pad, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)nq, s));
-    UMAP_TRY(prep_bf16(Xq, nq, d, d_pad, colsum.as<double>(), nr, xq16.as<__nv_bfloat16>(), qn.as<float>(), 1, s));
+    UMAP_TRY(prep_bf16(Xq, nq, d, d_pad, colsum.as<double>(), nr, xq16.as<__nv_bfloat16>(), qn.as<float>(), 1, s,
+                       pivot_order ? qperm : nullptr));
     const __nv_bfloat16* q16 = xq16.as<__nv_bfloat16>();
     const float* qnp = qn.as<float>();
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, q16, nq, d_pad, TC_BM));
     UMAP_TRY(make_map(&map_r, xr16.as<__nv_bfloat16>(), nr, d_pad, TC_BN / tc_cg()));
 
-    // reference splits so that the grid covers the GPU (split-R, like the exact kernel)
+    // reference splits so that the grid covers the GPU (split-R, like the exact kernel); none in
+    // pivot order (the self-column table indexes the whole reference range)
     const int64_t qblocks = (nq + TC_BM - 1) / TC_BM;
     int64_t splits = std::max<int64_t>(1, (num_sms() + qblocks - 1) / qblocks);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, nr / (4 * TC_BN)));
+    if (pivot_order) splits = 1;
     int64_t split_len = (nr + splits - 1) / splits;
     split_len = (split_len + TC_BN - 1) / TC_BN * TC_BN;
     const int n_splits = (int)((nr + split_len - 1) / split_len);
@@ -1240,7 +1365,12 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     a.prefilter = a.kblocks <= 4 ? 1 : 0;  // K <= 256: the epilogue, not the MMA, bounds the tile
     if (const char* e = getenv("UMAP_TC_PREFILTER")) a.prefilter = atoi(e);  // tuning knob
     a.split_len = split_len; a.self_shift = self_shift; a.exclude_self = exclude_self;
-    a.index_offset = index_offset; a.cand_idx = ci.as<int32_t>(); a.cand_d2 = cd.as<float>();
+    a.index_offset = pivot_order ? 0 : index_offset; a.cand_idx = ci.as<int32_t>(); a.cand_d2 = cd.as<float>();
+    if (pivot_order) {
+        a.self_shift = 0;  // self case: the same order on both sides; otherwise the self-column table
+        a.self_col = (exclude_self && !self_case) ? selfc.as<int32_t>() : nullptr;
+        a.rotate = getenv("UMAP_TC_KNN_NO_ROT") ? 0 : 1;  // A/B knob
+    }
     {
         const char* dbg = unsafe_env("UMAP_TC_DEBUG");
         a.debug = dbg ? atoi(dbg) : 0;
@@ -1250,7 +1380,15 @@ umap_status knn_tensor(const float* Xq, int64_t nq, const float* Xr, int64_t nr,
     else UMAP_TRY((launch_tc<64, 0>(map_q, map_r, a, grid, s)));
     const int32_t* cand = ci.as<int32_t>();
     Scratch mi, md;
-    if (n_splits > 1) {  // merge the per-split candidate lists by approximate key
+    if (pivot_order) {  // candidates back to the caller's row order and ids
+        UMAP_TRY(mi.alloc(sizeof(int32_t) * (size_t)nq * kc, s));
+        UMAP_TRY(md.alloc(sizeof(float) * (size_t)nq * kc, s));
+        unpermute_cand_kernel<<<(unsigned)ceil_div(nq * kc, 256), 256, 0, s>>>(
+            ci.as<int32_t>(), cd.as<float>(), qperm, rperm.as<int32_t>(), nq, kc, index_offset, mi.as<int32_t>(),
+            md.as<float>());
+        UMAP_LAUNCH_CHECK("unpermute_cand_kernel");
+        cand = mi.as<int32_t>();
+    } else if (n_splits > 1) {  // merge the per-split candidate lists by approximate key
         UMAP_TRY(mi.alloc(sizeof(int32_t) * (size_t)nq * kc, s));
         UMAP_TRY(md.alloc(sizeof(float) * (size_t)nq * kc, s));
         UMAP_TRY(topk_merge(ci.as<int32_t>(), cd.as<float>(), n_splits, nq, kc, kc, 1, mi.as<int32_t>(),
