@@ -23,7 +23,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 
 # per-file flags: the SGD kernels flush fp32 denormals (no range fix-ups around MUFU.LG2/RCP;
 # the layout's squared distances are either 0 or far above the denormal range, R12)
-PER_FILE = {"sgd.cu": ["-ftz=true"]}
+PER_FILE = {f: ["-ftz=true"] for f in ("sgd.cu", "sgd_persistent.cu", "transform.cu")}
 
 
 def _stale(target, deps):
