@@ -60,7 +60,8 @@ static const char* const k_prof_names[PROF_NSLOTS] = {
     "thresholds_warp_kernel", "grid_knn_kernel", "smooth_knn_kernel", "fuzzy union (5 kernels)",
     "sgd_kernel", "dist_tile_kernel (kNN, exact)", "dist_tile_kernel (trust, exact)",
     "transform_sgd_kernel", "knn_tc_kernel (trust coarse)", "spectral init (3 kernels x iterations)",
-    "trust projection (basis + operands)", "trust regroup + chunking", "kNN pivot order (short K)"};
+    "trust projection (basis + operands)", "trust regroup + chunking", "kNN pivot order (short K)",
+    "sgd schedule (count + fill)"};
 void count_launch(int n) { g_launches += n; }
 
 umap_status cuda_status(cudaError_t e, const char* what)

@@ -39,7 +39,7 @@ void count_launch(int n = 1);
 enum ProfSlot {
     PROF_KNN_TC = 0, PROF_RERANK, PROF_TRUST_TC, PROF_RANK_FIX, PROF_THRESHOLDS, PROF_GRID_KNN,
     PROF_SMOOTH_KNN, PROF_UNION, PROF_SGD, PROF_KNN_EXACT, PROF_TRUST_EXACT, PROF_TRANSFORM_SGD,
-    PROF_TRUST_COARSE, PROF_SPECTRAL, PROF_TRUST_PROJ, PROF_TRUST_REGROUP, PROF_KNN_PRUNE, PROF_NSLOTS
+    PROF_TRUST_COARSE, PROF_SPECTRAL, PROF_TRUST_PROJ, PROF_TRUST_REGROUP, PROF_KNN_PRUNE, PROF_SGD_SCHED, PROF_NSLOTS
 };
 bool profiling_enabled();
 void profile_record(int slot, cudaEvent_t e0, cudaEvent_t e1);

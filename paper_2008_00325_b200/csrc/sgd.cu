@@ -24,6 +24,7 @@
 // epoch; Hogwild reads are unsynchronised by definition (staleness bounded to one epoch).
 #include <cstdlib>
 
+#include "bulk.cuh"
 #include "sgd_common.cuh"
 
 namespace umapb200 {
@@ -435,6 +436,421 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
     if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
 }
 
+// ---------------------------------------------------------------- flat5: records in shared memory
+// flat3 with the CTA's records resident in shared memory for all epochs (SoA: r fp32, packed
+// hl << 21 | t), so the per-epoch scan (A) reads shared memory instead of streaming 8 bytes per
+// record from L2 every epoch; the due lists hold 16-bit record indices.  Same edge work, batches
+// and fixed-point sums as flat3 (R13: Y is bit-identical).
+template <int DIM, int MC>
+__global__ void __launch_bounds__(1024, 1) sgd_flat5_kernel(SgdArgs A)
+{
+    extern __shared__ __align__(16) unsigned char sgd_smem[];
+    const int vt = A.vt;         // >= the largest CTA range (multiple of 32)
+    const int cap = A.list_cap;  // >= the largest CTA record count (multiple of 32)
+    uint32_t* acc_lo = reinterpret_cast<uint32_t*>(sgd_smem);                  // [DIM][vt]
+    int32_t* acc_hi = reinterpret_cast<int32_t*>(acc_lo + (size_t)DIM * vt);     // [DIM][vt]
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(sgd_smem);  // wide mode: [DIM][vt]
+    float* yhead = reinterpret_cast<float*>(acc_hi + (size_t)DIM * vt);         // [vt][DIM]
+    float* rr = yhead + (size_t)DIM * vt;                                       // [cap] r
+    uint32_t* rx = reinterpret_cast<uint32_t*>(rr + cap);                       // [cap] hl << 21 | t
+    uint16_t* list0 = reinterpret_cast<uint16_t*>(rx + cap);                    // [2][cap] record indices
+    __shared__ int s_step, s_cur[2], s_nlist;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v_lo = A.bounds[blockIdx.x], v_hi = A.bounds[blockIdx.x + 1];
+    const int np = v_hi - v_lo;
+    const bool wide = *A.max_row > 65535;
+    const uint32_t nn = (uint32_t)A.n;
+    const int64_t E0 = __ldg(A.indptr + v_lo), E1 = __ldg(A.indptr + v_hi);
+    const int R = (int)(E1 - E0);
+    const int n_steps = (R + 31) >> 5;
+    unsigned long long due_count = 0;
+
+    constexpr int SG = 8;
+    auto scan = [&](int e, int buf, int limit) {
+        const float ef = (float)e, ef1 = (float)(e - 1);
+        uint16_t* list = list0 + (size_t)buf * cap;
+        int g = 0;
+        if (lane == 0) g = atomicAdd(&s_step, SG);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        while (g < limit) {
+            int gn = 0;
+            if (lane == 0) gn = atomicAdd(&s_step, SG);
+            unsigned ballot[SG];
+            int tot = 0;
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                const int i = 32 * (g + k) + lane;
+                const bool due = g + k < limit && i < R && edge_due_f(rr[i], ef, ef1);
+                ballot[k] = __ballot_sync(0xffffffffu, due);
+                tot += __popc(ballot[k]);
+            }
+            due_count += tot;
+            int base = 0;
+            if (lane == 0 && tot) base = atomicAdd(&s_cur[buf], tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+            for (int k = 0; k < SG; ++k) {
+                if ((ballot[k] >> lane) & 1u) list[base + __popc(ballot[k] & ((1u << lane) - 1u))] = (uint16_t)(32 * (g + k) + lane);
+                base += __popc(ballot[k]);
+            }
+            g = __shfl_sync(0xffffffffu, gn, 0);
+        }
+    };
+    int split = n_steps;
+    {
+        const int pct = A.scan_split_pct;
+        split = (int)(((int64_t)n_steps * pct / 100 + SG - 1) / SG * SG);
+        if (split > n_steps) split = n_steps;
+    }
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+        int2 rec;
+        if (A.prec) {
+            rec = ld_stream_i2(A.prec + E0 + i);
+        } else {
+            rec = ld_stream_i2(A.edges + E0 + i);
+            rec.x |= ld_stream_u16(A.hoff + E0 + i) << 21;
+        }
+        rr[i] = __int_as_float(rec.y);
+        rx[i] = (uint32_t)rec.x;
+    }
+    for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(A.Y0 + (int64_t)v_lo * DIM + i);
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            if (wide) acc64[c * vt + i] = 0ull;
+            else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+        }
+    }
+    if (threadIdx.x == 0) { s_step = 0; s_cur[0] = 0; s_cur[1] = 0; }
+    __syncthreads();
+    scan(A.e_begin, A.e_begin & 1, n_steps);
+    __syncthreads();
+    if (threadIdx.x == 0) { s_nlist = s_cur[A.e_begin & 1]; s_step = 0; }
+    __syncthreads();
+
+    for (int epoch = A.e_begin; epoch < A.e_end; ++epoch) {
+        const int par = (epoch - A.e_begin) & 1;
+        const float* Yr = par ? A.Y1 : A.Y0;
+        float* Yw = par ? A.Y0 : A.Y1;
+        const TermK K = epoch_terms(A, epoch);
+        const int buf = epoch & 1;
+        const uint16_t* list = list0 + (size_t)buf * cap;
+        const int nl = s_nlist;
+        const int nb = (nl + 31) >> 5;
+        // static strided batches (flat3): warp w takes batches w, w + 32, ...
+        for (int b = warp; b < nb; b += 32) {
+            const int j = b + lane * nb;
+            const bool act = j < nl;
+            const uint32_t ent = act ? rx[list[j]] : 0u;
+            const int hl = (int)(ent >> 21), t = act ? (int)(ent & 0x1FFFFFu) : v_lo;
+            int qa[DIM];
+            edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, hl, t, act, qa);
+            if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
+        }
+        if (epoch + 1 < A.e_end) scan(epoch + 1, buf ^ 1, split);
+        __syncthreads();
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            const int v = v_lo + i;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                long long tot;
+                if (wide) { tot = (long long)acc64[c * vt + i]; acc64[c * vt + i] = 0ull; }
+                else {
+                    tot = (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
+                    acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0;
+                }
+                const float y = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
+                yhead[i * DIM + c] = y;
+                Yw[(int64_t)v * DIM + c] = y;
+            }
+        }
+        if (epoch + 1 < A.e_end) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.bar) : "memory");
+                s_step = split;
+            }
+            __syncthreads();
+            scan(epoch + 1, buf ^ 1, n_steps);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_nlist = s_cur[buf ^ 1]; s_cur[buf] = 0; s_step = 0;
+                const unsigned int target = (unsigned int)(epoch - A.e_begin + 1) * gridDim.x;
+                unsigned int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.bar) : "memory");
+                } while (v < target);
+            }
+            __syncthreads();
+        } else {
+            __syncthreads();
+        }
+    }
+    if (A.positives && lane == 0 && due_count) atomicAdd(A.positives, due_count);
+}
+
+// ---------------------------------------------------------------- flat4: materialised schedule
+// The schedule (R9) does not depend on the positions, so every CTA's due lists are built before
+// the launch and the epoch loop streams them instead of scanning every record every epoch
+// (flat3's scan: ~1 ms of the 7.4 ms at C2, tools/sgd_decomp.py; the records cost 8 bytes of
+// L2->SM traffic per record per epoch, a due entry 4 bytes per due edge).
+//
+// Layout: a CTA range's records are cut into slots of SK_SLOT consecutive records (CSR order);
+// slot s owns a region of the list array, epoch-major: for each epoch its due records (packed
+// hl << 21 | t) in CSR order, padded with SK_PAD entries to a multiple of 4 (16-byte bulk copies),
+// and pcnt[b][i][s] = that padded count.  The region bound is exact: the records due in epochs
+// [e_begin, e_end) number at most floor(fl((e_end - 1) r)) - floor(fl((e_begin - 1) r)) per record
+// (fl(e r) is monotone in e; the due test counts the strict increases of its floor).
+//
+// sgd_flat4_kernel: per epoch, warp 0 fetches the CTA's slot segments of epoch e + 2 into one
+// shared-memory list with the TMA bulk-copy engine (one cp.async.bulk per slot, completion on the
+// buffer's mbarrier) while epochs e and e + 1 run; the padded counts of epoch e + 2 are fetched by
+// LDGSTS at the start of epoch e.  Edge work, batches and fixed-point sums are flat3's (R13: Y is
+// bit-identical); padding entries are inactive lanes.
+// records per slot: SK_SLOT_MIN x 2^j (tuning knob UMAP_SGD_SLOT; one warp holds a slot's records in registers)
+constexpr int SK_SLOT_MIN = 256;
+constexpr int SK_MAXSLOTS = 128;    // slots per CTA range handled by flat4 (C2: 42)
+constexpr uint32_t SK_PAD = 0xFFFFFFFFu;
+
+// per CTA range b: its slot count
+__global__ void sched_slots_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ bounds, int G,
+                                   int slot, int32_t* __restrict__ nslots)
+{
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= G) return;
+    const int64_t R = indptr[bounds[b + 1]] - indptr[bounds[b]];
+    nslots[b] = (int32_t)((R + slot - 1) / slot);
+}
+
+// per slot (one warp): its CTA range (slot_b) and the region bound (records' due epochs + padding)
+__global__ void sched_bound_kernel(const int2* __restrict__ prec, const int64_t* __restrict__ indptr,
+                                   const int32_t* __restrict__ bounds, int G, const int64_t* __restrict__ slot_base,
+                                   int64_t S, int slot, int e_begin, int e_end, int32_t* __restrict__ slot_b,
+                                   int64_t* __restrict__ bound)
+{
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= S) return;
+    int lo = 0, hi = G - 1;  // last b with slot_base[b] <= gw
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (slot_base[mid] <= gw) lo = mid; else hi = mid - 1;
+    }
+    const int b = lo;
+    const int64_t E0 = indptr[bounds[b]] + (gw - slot_base[b]) * slot;
+    const int64_t E1 = min(indptr[bounds[b + 1]], E0 + slot);
+    const float ea = (float)(e_begin - 1), ez = (float)(e_end - 1);
+    int64_t c = 0;
+    for (int64_t e = E0 + lane; e < E1; e += 32) {
+        const float r = __int_as_float(prec[e].y);
+        c += (int64_t)(floorf(__fmul_rn(ez, r)) - floorf(__fmul_rn(ea, r)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) {
+        slot_b[gw] = b;
+        bound[gw] = (c + 3LL * (e_end - e_begin) + 3) & ~3LL;  // regions start 16-byte aligned
+    }
+}
+
+// one warp per slot of 32 MS records: the due lists of every epoch into the slot's region,
+// pcnt[b][i][s] = padded count.  Due test: floor(fl(e r)) > floor(fl((e - 1) r))  <=>
+// floor(fl(e r)) > fl((e - 1) r).  Branch-free: ballot, prefix popc, predicated store.
+template <int MS>
+__global__ void __launch_bounds__(256)
+sched_fill_kernel(const int2* __restrict__ prec, const int64_t* __restrict__ indptr, const int32_t* __restrict__ bounds,
+                  const int64_t* __restrict__ slot_base, const int32_t* __restrict__ slot_b, int64_t S, int e_begin,
+                  int NE, const int64_t* __restrict__ region, int32_t* __restrict__ pcnt, uint32_t* __restrict__ out)
+{
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= S) return;
+    const int b = slot_b[gw];
+    const int64_t sb = slot_base[b];
+    const int local = (int)(gw - sb), ns = (int)(slot_base[b + 1] - sb);
+    const int64_t E0 = indptr[bounds[b]] + (int64_t)local * (32 * MS);
+    const int64_t E1 = min(indptr[bounds[b + 1]], E0 + 32 * MS);
+    float r[MS], pv[MS];
+    uint32_t x[MS];
+    const float ef0 = (float)(e_begin - 1);
+#pragma unroll
+    for (int k = 0; k < MS; ++k) {
+        const int64_t e = E0 + 32 * k + lane;
+        const int2 rc = e < E1 ? prec[e] : make_int2(0, 0);  // r = 0: never due
+        r[k] = __int_as_float(rc.y);
+        x[k] = (uint32_t)rc.x;
+        pv[k] = __fmul_rn(ef0, r[k]);
+    }
+    uint32_t* o = out + region[gw];
+    int32_t* pc = pcnt + (int64_t)NE * sb + local;
+    unsigned lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    for (int i = 0; i < NE; ++i) {
+        const float ef = (float)(e_begin + i);
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < MS; ++k) {
+            const float xe = __fmul_rn(ef, r[k]);
+            const bool due = floorf(xe) > pv[k];
+            pv[k] = xe;
+            const unsigned bal = __ballot_sync(0xffffffffu, due);
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p st.global.u32 [%0], %1;\n\t}"
+                         ::"l"(o + c + __popc(bal & lt)), "r"(x[k]), "r"((int)due) : "memory");
+            c += __popc(bal);
+        }
+        const int pad = (4 - (c & 3)) & 3;
+        if (lane < pad) o[c + lane] = SK_PAD;
+        c += pad;
+        if (lane == 0) pc[(int64_t)i * ns] = c;
+        o += c;
+    }
+}
+
+template <int DIM, int MC>
+__global__ void __launch_bounds__(1024, 1) sgd_flat4_kernel(SgdArgs A)
+{
+    extern __shared__ __align__(16) unsigned char sgd_smem[];
+    const int vt = A.vt;         // >= the largest CTA range, multiple of 32
+    const int cap = A.list_cap;  // >= the largest padded epoch list, multiple of 32
+    uint32_t* acc_lo = reinterpret_cast<uint32_t*>(sgd_smem);                  // [DIM][vt]
+    int32_t* acc_hi = reinterpret_cast<int32_t*>(acc_lo + (size_t)DIM * vt);     // [DIM][vt]
+    unsigned long long* acc64 = reinterpret_cast<unsigned long long*>(sgd_smem);  // wide mode: [DIM][vt]
+    float* yhead = reinterpret_cast<float*>(acc_hi + (size_t)DIM * vt);         // [vt][DIM]
+    uint32_t* list0 = reinterpret_cast<uint32_t*>(yhead + (size_t)DIM * vt);    // [2][cap], 16-byte aligned
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ int64_t s_src[SK_MAXSLOTS];  // next unread entry of each slot's region
+    __shared__ int32_t s_pc[2][SK_MAXSLOTS];
+    __shared__ int s_nl[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int v_lo = A.bounds[blockIdx.x], v_hi = A.bounds[blockIdx.x + 1];
+    const int np = v_hi - v_lo;
+    const bool wide = *A.max_row > 65535;
+    const uint32_t nn = (uint32_t)A.n;
+    const int NE = A.e_end - A.e_begin;
+    const int64_t sb = A.slot_base[blockIdx.x];
+    const int ns = (int)(A.slot_base[blockIdx.x + 1] - sb);
+    const int32_t* pcb = A.sched_pcnt + (int64_t)NE * sb;
+    const uint32_t bar0 = smem_u32(&s_bar[0]);
+    // warp 0: LDGSTS of the padded counts of epoch index i into s_pc[i & 1]
+    auto fetch_counts = [&](int i) {
+        for (int s = lane; s < ns; s += 32) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&s_pc[i & 1][s])),
+                         "l"(pcb + (int64_t)i * ns + s) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // warp 0: bulk copies of the slot segments of epoch index i into list buffer i & 1 (counts in
+    // s_pc[i & 1], complete: cp.async.wait_all + __syncwarp by the caller)
+    auto fetch_lists = [&](int i) {
+        const int bi = i & 1;
+        const uint32_t bar = bar0 + 8u * (uint32_t)bi;
+        const uint32_t dst0 = smem_u32(list0 + (size_t)bi * cap);
+        int base = 0;
+        int pcs[SK_MAXSLOTS / 32], offs[SK_MAXSLOTS / 32];
+#pragma unroll
+        for (int q = 0; q < SK_MAXSLOTS / 32; ++q) {
+            const int s = lane + 32 * q;
+            const int c = s < ns ? s_pc[bi][s] : 0;
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            pcs[q] = c;
+            offs[q] = base + incl - c;
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) {
+            s_nl[bi] = base;
+            mbar_expect_tx(bar, (uint32_t)base * 4u);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < SK_MAXSLOTS / 32; ++q) {
+            const int s = lane + 32 * q;
+            if (pcs[q] > 0) {
+                bulk_g2s(dst0 + (uint32_t)offs[q] * 4u, A.sched + s_src[s], (uint32_t)pcs[q] * 4u, bar);
+                s_src[s] += pcs[q];
+            }
+        }
+    };
+    if (warp == 0) {
+        for (int s = lane; s < ns; s += 32) s_src[s] = A.sched_region[sb + s];
+        if (lane == 0) {
+            mbar_init(bar0, 1);
+            mbar_init(bar0 + 8, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        fetch_counts(0);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        fetch_lists(0);
+        if (NE > 1) fetch_counts(1);
+    }
+    for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(A.Y0 + (int64_t)v_lo * DIM + i);
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            if (wide) acc64[c * vt + i] = 0ull;
+            else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+        }
+    }
+    __syncthreads();
+    unsigned long long due_count = 0;
+    for (int ie = 0; ie < NE; ++ie) {
+        const int epoch = A.e_begin + ie;
+        const float* Yr = (ie & 1) ? A.Y1 : A.Y0;
+        float* Yw = (ie & 1) ? A.Y0 : A.Y1;
+        const TermK K = epoch_terms(A, epoch);
+        const uint32_t* list = list0 + (size_t)(ie & 1) * cap;
+        const int nl = s_nl[ie & 1];
+        const int nb = (nl + 31) >> 5;
+        if (warp == 0 && ie + 1 < NE) {
+            // list buffer (ie + 1) & 1 was last read in epoch ie - 1 (grid barrier since): order
+            // those generic reads before the async-proxy refill; its counts arrived by LDGSTS
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+            fetch_lists(ie + 1);
+            if (ie + 2 < NE) fetch_counts(ie + 2);  // s_pc[ie & 1] was consumed by fetch_lists(ie)
+        }
+        mbar_wait(bar0 + 8u * (uint32_t)(ie & 1), (uint32_t)(ie >> 1) & 1u);
+        // warp w takes the strided batches 31 - w, 63 - w, ...: batch b = entries b, b + nb, ...
+        // (the slots' CSR order: 32 different heads per batch, flat3); padding entries are
+        // inactive; warp 0, which issues the fetches, gets the last batch only when nb % 32 == 0
+        for (int b = 31 - warp; b < nb; b += 32) {
+            const int j = b + lane * nb;
+            const uint32_t ent = j < nl ? list[j] : SK_PAD;
+            const bool act = ent != SK_PAD;
+            due_count += act;
+            const int hl = (int)(ent >> 21), t = act ? (int)(ent & 0x1FFFFFu) : v_lo;
+            int qa[DIM];
+            edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, act ? hl : 0, t, act, qa);
+            if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
+            const int v = v_lo + i;
+#pragma unroll
+            for (int c = 0; c < DIM; ++c) {
+                long long tot;
+                if (wide) { tot = (long long)acc64[c * vt + i]; acc64[c * vt + i] = 0ull; }
+                else {
+                    tot = (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
+                    acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0;
+                }
+                const float y = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
+                yhead[i * DIM + c] = y;
+                Yw[(int64_t)v * DIM + c] = y;
+            }
+        }
+        if (ie + 1 < NE) grid_barrier(A.bar, (unsigned int)(ie + 1));
+        else __syncthreads();
+    }
+    if (A.positives && due_count) atomicAdd(A.positives, due_count);
+}
+
 // Expected per-epoch cost of vertex v's work in the flat kernel, in units of 1/256 record
 // scan: every record is scanned each epoch, record e is due in a fraction ~r_e of the epochs
 // (R9) and then costs cdue scans' worth (the gathers and the gradient), plus cvert for the
@@ -538,6 +954,15 @@ __global__ void cta_extent_kernel(const int64_t* __restrict__ indptr, const int3
     atomicMax(out + 1, rec > INT32_MAX ? INT32_MAX : (int)rec);
 }
 
+// tuning knob UMAP_SGD_SCHED: 0 = flat3 (records streamed from L2 every epoch), 1 = flat4
+// (materialised schedule), 2 = flat5 (records in shared memory; default)
+int sgd_sched_mode()
+{
+    const char* e = getenv("UMAP_SGD_SCHED");
+    return e ? atoi(e) : 2;
+}
+bool sgd_sched_enabled() { return sgd_sched_mode() == 1; }
+
 // ver: 1 = the round-1 flat kernel, 2 = flat2, 3 = flat3 when every CTA range fits one piece
 // (else flat2)
 template <int DIM, int MC>
@@ -619,7 +1044,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
             }
         }
     }
-    static PerDeviceOnce attr[4];
+    static PerDeviceOnce attr[5];
     if ((A.debug & ~3) != 0) {
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -649,10 +1074,87 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
         UMAP_LAUNCH_CHECK("pack_records_kernel");
         A.prec = prec.as<int2>();
     }
+    // flat4: materialise the schedule (R9) when the packed records exist, every CTA range has at
+    // most SK_MAXSLOTS slots and the lists fit in half the free device memory (C2: 0.9 GB); else
+    // flat3's in-kernel scan
+    Scratch sched, nsl, sbase, slotb, sbound, sregion, pcnt;
+    int slot = SK_SLOT_MIN * 2;
+    if (const char* e = getenv("UMAP_SGD_SLOT")) slot = atoi(e) >= 1024 ? 1024 : atoi(e) >= 512 ? 512 : 256;  // tuning knob
+    if (ver == 3 && A.prec && sgd_sched_enabled() && (int64_t)A.list_cap <= (int64_t)SK_MAXSLOTS * slot) {
+        const int NE = A.e_end - A.e_begin;
+        UMAP_TRY(nsl.alloc(sizeof(int32_t) * (size_t)grid, s));
+        UMAP_TRY(sbase.alloc(sizeof(int64_t) * (size_t)(grid + 1), s));
+        int64_t S = 0, total = 0;
+        {
+            ProfScope pc(PROF_SGD_SCHED, s);
+            sched_slots_kernel<<<ceil_div(grid, 256), 256, 0, s>>>(A.indptr, bounds.as<int32_t>(), grid, slot,
+                                                                  nsl.as<int32_t>());
+            UMAP_LAUNCH_CHECK("sched_slots_kernel");
+            UMAP_TRY(exclusive_scan<int32_t>(nsl.as<int32_t>(), grid, sbase.as<int64_t>(), s));
+        }
+        UMAP_CUDA_TRY(cudaMemcpyAsync(&S, sbase.as<int64_t>() + grid, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        UMAP_TRY(slotb.alloc(sizeof(int32_t) * (size_t)S, s));
+        UMAP_TRY(sbound.alloc(sizeof(int64_t) * (size_t)S, s));
+        UMAP_TRY(sregion.alloc(sizeof(int64_t) * (size_t)(S + 1), s));
+        {
+            ProfScope pc(PROF_SGD_SCHED, s);
+            sched_bound_kernel<<<ceil_div(S * 32, 256), 256, 0, s>>>(A.prec, A.indptr, bounds.as<int32_t>(), grid,
+                                                                    sbase.as<int64_t>(), S, slot, A.e_begin, A.e_end,
+                                                                    slotb.as<int32_t>(), sbound.as<int64_t>());
+            UMAP_LAUNCH_CHECK("sched_bound_kernel");
+            UMAP_TRY(exclusive_scan<int64_t>(sbound.as<int64_t>(), S, sregion.as<int64_t>(), s));
+        }
+        UMAP_CUDA_TRY(cudaMemcpyAsync(&total, sregion.as<int64_t>() + S, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        size_t free_b = 0, total_b = 0;
+        UMAP_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+        const size_t smem4 = smem + 2 * sizeof(uint32_t) * (size_t)(3 * SK_MAXSLOTS + 32);
+        if ((size_t)total * 4 <= free_b / 2 && smem4 <= 200 * 1024) {
+            UMAP_TRY(sched.alloc(sizeof(uint32_t) * (size_t)total, s));
+            UMAP_TRY(pcnt.alloc(sizeof(int32_t) * (size_t)S * NE, s));
+            ProfScope pf(PROF_SGD_SCHED, s);
+            auto fill = slot == 1024 ? sched_fill_kernel<32> : slot == 512 ? sched_fill_kernel<16> : sched_fill_kernel<8>;
+            fill<<<ceil_div(S * 32, 256), 256, 0, s>>>(A.prec, A.indptr, bounds.as<int32_t>(), sbase.as<int64_t>(),
+                                                      slotb.as<int32_t>(), S, A.e_begin, NE, sregion.as<int64_t>(),
+                                                      pcnt.as<int32_t>(), sched.as<uint32_t>());
+            UMAP_LAUNCH_CHECK("sched_fill_kernel");
+            A.sched = sched.as<uint32_t>();
+            A.slot_base = sbase.as<int64_t>();
+            A.sched_region = sregion.as<int64_t>();
+            A.sched_pcnt = pcnt.as<int32_t>();
+            // a padded epoch list holds at most the CTA's records + 3 per slot
+            A.list_cap = (A.list_cap + 3 * SK_MAXSLOTS + 31) & ~31;
+            smem = smem4;
+            ver = 4;
+            kern = sgd_flat4_kernel<DIM, MC>;
+            if (attr[4].first()) {
+                UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                   (int)cudaSharedmemCarveoutMaxL1));
+            }
+        }
+    }
+    if (ver == 3 && sgd_sched_mode() == 2) {
+        // flat5: records (8 B) and 16-bit list entries (2 x 2 B) per record instead of 2 x 4 B
+        const size_t smem5 = (size_t)(sizeof(unsigned long long) + sizeof(float)) * DIM * A.vt +
+                             (size_t)A.list_cap * (sizeof(float) + sizeof(uint32_t) + 2 * sizeof(uint16_t));
+        if (smem5 <= 200 * 1024 && A.list_cap <= 65535) {
+            smem = smem5;
+            ver = 5;
+            kern = sgd_flat5_kernel<DIM, MC>;
+            static PerDeviceOnce attr5;
+            if (attr5.first()) {
+                UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                   (int)cudaSharedmemCarveoutMaxL1));
+            }
+        }
+    }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
     UMAP_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(nt), args, smem, s));
-    UMAP_LAUNCH_CHECK(ver == 3 ? "sgd_flat3_kernel" : ver == 2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
+    UMAP_LAUNCH_CHECK(ver == 5 ? "sgd_flat5_kernel" : ver == 4 ? "sgd_flat4_kernel" : ver == 3 ? "sgd_flat3_kernel" : ver == 2 ? "sgd_flat2_kernel" : "sgd_flat_kernel");
     return UMAP_OK;
 }
 

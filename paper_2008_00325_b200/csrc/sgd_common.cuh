@@ -35,6 +35,14 @@ struct SgdArgs {
     int list_cap;            // flat3: due-list capacity (>= every CTA's record count)
     int scan_split_pct;      // flat3: % of the next epoch's scan done before the grid barrier's arrive
     int batch_static;        // flat3: 1 = warp w takes batches w, w + 32, ... (0: claimed dynamically)
+    // flat4: the closed-form schedule (R9) materialised before the launch (sgd.cu, flat4): CTA b's
+    // records in slots [slot_base[b], slot_base[b + 1]); slot s's epoch lists start at
+    // sched + sched_region[s], the padded count of epoch index i at
+    // sched_pcnt[NE slot_base[b] + i (slots of b) + (s - slot_base[b])]
+    const uint32_t* sched;
+    const int64_t* slot_base;
+    const int64_t* sched_region;
+    const int32_t* sched_pcnt;
 };
 
 __device__ __forceinline__ u32x4 philox_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const SgdArgs& A)

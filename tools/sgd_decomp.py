@@ -35,6 +35,8 @@ for v in variants:
         pos = U.optimize(indptr, col, val, Y, 1, 500, n_epochs=500, a=a, b=b, seed=1, sgd_mode="deterministic")
         p = U.profile_end()
         ts.append(p["sgd_kernel"][0])
+        sch = p.get("sgd schedule (count + fill)", (0.0, 0))[0]
     h = hashlib.sha1(Y.cpu().numpy().tobytes()).hexdigest()[:16]
-    print(json.dumps({"debug": v, "sgd_ms": [round(t, 3) for t in ts[1:]], "positives": pos, "sha1": h}), flush=True)
+    print(json.dumps({"debug": v, "sgd_ms": [round(t, 3) for t in ts[1:]], "sched_ms": round(sch, 3), "positives": pos, "sha1": h,
+                      "sched_mode": os.environ.get("UMAP_SGD_SCHED", "2")}), flush=True)
 os.environ.pop("UMAP_SGD_DEBUG", None)
