@@ -441,8 +441,8 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
 // hl << 21 | t), so the per-epoch scan (A) reads shared memory instead of streaming 8 bytes per
 // record from L2 every epoch; the due lists hold 16-bit record indices.  Same edge work, batches
 // and fixed-point sums as flat3 (R13: Y is bit-identical).
-template <int DIM, int MC>
-__global__ void __launch_bounds__(1024, 1) sgd_flat5_kernel(SgdArgs A)
+template <int DIM, int MC, int NT = 1024, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) sgd_flat5_kernel(SgdArgs A)
 {
     extern __shared__ __align__(16) unsigned char sgd_smem[];
     const int vt = A.vt;         // >= the largest CTA range (multiple of 32)
@@ -537,8 +537,8 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat5_kernel(SgdArgs A)
         const uint16_t* list = list0 + (size_t)buf * cap;
         const int nl = s_nlist;
         const int nb = (nl + 31) >> 5;
-        // static strided batches (flat3): warp w takes batches w, w + 32, ...
-        for (int b = warp; b < nb; b += 32) {
+        // static strided batches (flat3): warp w takes batches w, w + NT / 32, ...
+        for (int b = warp; b < nb; b += NT / 32) {
             const int j = b + lane * nb;
             const bool act = j < nl;
             const uint32_t ent = act ? rx[list[j]] : 0u;
@@ -966,9 +966,15 @@ bool sgd_sched_enabled() { return sgd_sched_mode() == 1; }
 // ver: 1 = the round-1 flat kernel, 2 = flat2, 3 = flat3 when every CTA range fits one piece
 // (else flat2)
 template <int DIM, int MC>
-umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
+umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver, int cps_req, bool* retry)
 {
-    const int grid = num_sms();  // one CTA of 32 warps per SM (checked against the occupancy below)
+    // one CTA of 32 warps per SM, or (flat5, cps_req = 2, the default) two CTAs of 18 warps per SM:
+    // 36 warps at <= 56 registers carry 1152 due edges per round instead of 1024 (C2: ~3,090 due
+    // edges per SM per epoch take 3 rounds on every SM instead of 4 on about half of them; the
+    // grid barrier waits for the slowest).  *retry: the flat5 two-CTA form does not fit, call
+    // again with cps_req = 1.
+    const int cps = (ver == 3 && sgd_sched_mode() == 2 && cps_req == 2) ? 2 : 1;
+    const int grid = num_sms() * cps;
     A.n_chunks = A.n;
     Scratch bounds, hoff;
     UMAP_TRY(bounds.alloc(sizeof(int32_t) * (size_t)(grid + 1), s));
@@ -1029,7 +1035,7 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
         const size_t per_v = (sizeof(unsigned long long) + (ver == 2 ? sizeof(float) : 0)) * (size_t)DIM;
         smem = per_v * A.vt + QBYTES;
     }
-    const int nt = 1024;
+    int nt = 1024;
     auto kern = ver == 3 ? sgd_flat3_kernel<DIM, MC>
             : ver == 2 ? sgd_flat2_kernel<DIM, MC> : sgd_flat_kernel<DIM, MC>;
     if constexpr (DIM == 2 && MC == 5) {  // timing-decomposition variants (unsafe experiments only)
@@ -1142,14 +1148,29 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver)
         if (smem5 <= 200 * 1024 && A.list_cap <= 65535) {
             smem = smem5;
             ver = 5;
-            kern = sgd_flat5_kernel<DIM, MC>;
-            static PerDeviceOnce attr5;
-            if (attr5.first()) {
+            kern = cps == 2 ? sgd_flat5_kernel<DIM, MC, 576, 2> : sgd_flat5_kernel<DIM, MC>;
+            nt = cps == 2 ? 576 : 1024;
+            static PerDeviceOnce attr5[2];
+            if (attr5[cps - 1].first())
                 UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                                   (int)cudaSharedmemCarveoutMaxL1));
+            // carveout: the smallest shared-memory share that holds cps CTAs (the rest is L1, which
+            // caches the gathered positions); set per launch (the size depends on the graph)
+            const int pct = cps == 1 ? (int)cudaSharedmemCarveoutMaxL1
+                                     : std::min(100, (int)((cps * (smem + 2048) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+            UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            int per5 = 0;
+            UMAP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per5, kern, nt, smem));
+            if (per5 < cps) {
+                if (retry) *retry = true;
+                set_last_error("flat5 SGD kernel: fewer resident CTAs per SM than the launch needs");
+                return UMAP_ERR_CUDA;
             }
         }
+    }
+    if (cps != 1 && ver != 5) {
+        if (retry) *retry = true;
+        set_last_error("two CTAs per SM need the flat5 kernel");
+        return UMAP_ERR_CUDA;
     }
     void* args[] = {&A};
     ProfScope ps(PROF_SGD, s);
@@ -1176,7 +1197,15 @@ umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
         if (det && (sv == 0 || sv == 100 || sv == 101)) {
             // 100: the round-1 flat kernel, 101: flat2 (A/B comparisons); default flat3 (else flat2)
             const int ver = sv == 100 ? 1 : sv == 101 ? 2 : 3;
-            return A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver) : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver);
+            // tuning knob UMAP_SGD_CPS=1: flat5 as one CTA of 32 warps per SM
+            const int cps = (getenv("UMAP_SGD_CPS") && atoi(getenv("UMAP_SGD_CPS")) == 1) ? 1 : 2;
+            bool retry = false;
+            umap_status st = A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver, cps, &retry)
+                                      : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver, cps, &retry);
+            if (st != UMAP_OK && retry)
+                st = A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver, 1, nullptr)
+                              : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver, 1, nullptr);
+            return st;
         }
     }
     return launch_sgd_persistent<DIM>(A, det, s);
