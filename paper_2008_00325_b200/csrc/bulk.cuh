@@ -31,9 +31,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the waiting thread is suspended in hardware until the phase
+// completes (or the hint, 10 ms, elapses) instead of re-issuing the poll: a spinning producer or
+// MMA thread otherwise takes issue slots from the epilogue warps of its scheduler
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
-    while (!mbar_try_wait(bar, parity)) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity), "r"(10000000u)
+            : "memory");
     }
 }
 

@@ -150,10 +150,10 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
     while (!ok) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(bar), "r"(parity)
+            : "r"(bar), "r"(parity), "r"(10000000u)
             : "memory");
     }
 }
@@ -211,6 +211,35 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// tcgen05.ld of 32 columns without the wait (issue several, then tmem_ld_wait)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, float (&v)[32])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// tcgen05.wait::ld with v as in/out operands, so that no use of v is scheduled before the wait
+// (a second call after the first is an immediate no-op that only orders the other array)
+__device__ __forceinline__ void tmem_ld_wait(float (&v)[32])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                   "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]),
+                   "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]), "+f"(v[22]), "+f"(v[23]),
+                   "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]), "+f"(v[28]), "+f"(v[29]), "+f"(v[30]), "+f"(v[31])
+                 :
+                 : "memory");
 }
 
 struct TcArgs {
@@ -317,6 +346,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                          ? (int)(((int64_t)pblk * 2 * TC_BM * ntiles_all / (a.nq > 0 ? a.nq : 1)) % ntiles_all) : 0;
     auto tile_at = [&](int t) { return tlist ? tlist[t] : (rot0 ? (t + rot0) % ntiles_all : t); };
     const int KB = a.kblocks;
+    // short K (single-part operands, KB <= 2 slabs: C4's d = 50, the projected coarse pass): the
+    // query block's A slabs are loaded once, with tile 0, into the A regions of stages 0..KB-1 and
+    // stay there; later tiles stream only B (halves the L2 -> SMEM bytes per tile at KB = 1)
+    const bool res_a = MODE != 1 && KB <= 2 && KB <= TC_STAGES;
 
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
     const uint32_t tfull0 = smem_u32(bars + 2 * TC_STAGES), tempty0 = smem_u32(bars + 2 * TC_STAGES + 2);
@@ -375,15 +408,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         mbar_wait(empty0 + 8 * s, ph ^ 1);
                         const uint32_t dst = smem_u32(stage_base + s * STAGE_C);
                         const int x = (part * KB + kb) * TC_BK;
+                        const bool load_a = !res_a || t == 0;
+                        const uint32_t bytes = load_a ? STAGE_C : STAGE_C - A_BYTES;
                         if constexpr (CG == 2) {
                             // both CTAs' bytes complete on the leader's full barrier
-                            if (leader) mbar_expect_tx(full0 + 8 * s, CG * STAGE_C);
+                            if (leader) mbar_expect_tx(full0 + 8 * s, CG * bytes);
                             const uint32_t fb = mapa_shared(full0 + 8 * s, 0);
-                            tma_load_2d_cg2(dst, &map_q, x, (int)q0, fb, pol_a);
+                            if (load_a) tma_load_2d_cg2(dst, &map_q, x, (int)q0, fb, pol_a);
                             tma_load_2d_cg2(dst + A_BYTES, &map_r, x, y_r + (int)(rank * B_ROWS), fb, pol_b);
                         } else {
-                            mbar_expect_tx(full0 + 8 * s, STAGE_C);
-                            tma_load_2d_hint(dst, &map_q, x, (int)q0, full0 + 8 * s, pol_a);
+                            mbar_expect_tx(full0 + 8 * s, bytes);
+                            if (load_a) tma_load_2d_hint(dst, &map_q, x, (int)q0, full0 + 8 * s, pol_a);
                             tma_load_2d_hint(dst + A_BYTES, &map_r, x, y_r, full0 + 8 * s, pol_b);
                         }
                     }
@@ -405,8 +440,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const uint32_t ph = (g / TC_STAGES) & 1;
                     mbar_wait(full0 + 8 * s, ph);
                     tc_fence_after();
-                    const uint32_t a_addr = smem_u32(stage_base + s * STAGE_C);
-                    const uint32_t b_addr = a_addr + A_BYTES;
+                    const uint32_t b_addr = smem_u32(stage_base + s * STAGE_C) + A_BYTES;
+                    const uint32_t a_addr = smem_u32(stage_base + (res_a ? kb : s) * STAGE_C);
 #pragma unroll
                     for (int kk = 0; kk < TC_BK / 16; ++kk) {
                         if (!(a.debug & 2)) umma_mma<CG>(tmem_d, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
@@ -656,28 +691,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             tc_fence_after();
             const int64_t rb = r_lo + (int64_t)tile_at(t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
-#pragma unroll 1
-            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 32) {
-                float v[32];
-                tmem_ld32(taddr + c, v);
-                const int64_t jb = rb + c;
-                // the accumulator holds -d2/2 (norms folded into the GEMM); out-of-range
-                // columns (zero-filled TMA rows) are masked by their index
+            // one chunk of 32 columns (jb = its first column): the columns that beat the running
+            // threshold, then one insertion round per candidate of the busiest lane; each lane
+            // inserts its lowest remaining candidate (selected from registers by a 5-level select tree)
+            auto chunk = [&](const float (&v)[32], int64_t jb) {
                 const float nthr = -0.5f * thr;
-                if (a.prefilter) {
-                    // short K (the epilogue bounds the kernel): most chunks hold no candidate for
-                    // any row of the warp; a max tree and one vote skip them before the
-                    // per-column mask is built
-                    float m16[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
-#pragma unroll
-                    for (int w = 8; w >= 1; w >>= 1) {
-#pragma unroll
-                        for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
-                    }
-                    if (!__any_sync(0xffffffffu, valid && m16[0] > nthr)) continue;
-                }
                 const int valid_cols = (int)imin64(32, r_hi - jb);
                 uint32_t cm = 0;  // columns of this chunk that beat the running threshold
 #pragma unroll
@@ -685,8 +703,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
                 if (!valid) cm = 0;
                 if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
-                // one insertion round per candidate of the busiest lane; each lane inserts its
-                // lowest remaining candidate (selected from registers by a 5-level select tree)
                 while (__any_sync(0xffffffffu, cm != 0)) {
                     const int u = cm ? __ffs(cm) - 1 : 0;
                     const bool has = cm != 0;
@@ -715,6 +731,41 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     }
                     thr = kd[KC - 1];
                 }
+            };
+            // 32-column chunk maximum (31-op tree): the accumulator holds -d2/2, so a chunk with
+            // max <= -thr/2 holds no candidate for this row
+            auto cmax = [](const float (&v)[32]) {
+                float m16[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+                for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+                    for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
+                }
+                return m16[0];
+            };
+            // two chunks per step: both TMEM loads in flight before one wait, two independent max
+            // trees (the short-K prefilter: most chunks hold no candidate for any row of the warp
+            // and are skipped after one vote); out-of-range columns (zero-filled TMA rows) are
+            // masked by their index
+#pragma unroll 1
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 64) {
+                float v0[32], v1[32];
+                tmem_ld32_nw(taddr + c, v0);
+                tmem_ld32_nw(taddr + c + 32, v1);
+                tmem_ld_wait(v0);
+                tmem_ld_wait(v1);
+                const int64_t jb = rb + c;
+                bool p0 = true, p1 = true;
+                if (a.prefilter) {
+                    const float nthr = -0.5f * thr;
+                    const float m0 = cmax(v0), m1 = cmax(v1);
+                    p0 = __any_sync(0xffffffffu, valid && m0 > nthr);
+                    p1 = __any_sync(0xffffffffu, valid && m1 > nthr);
+                }
+                if (p0) chunk(v0, jb);
+                if (p1) chunk(v1, jb + 32);
             }
             tc_fence_before();
             __syncwarp();
