@@ -180,6 +180,13 @@ def kernel_work(slot, c, st, n_amb, fine_frac=1.0, world=1):
     n, d, k, N, m, dim = c["n"], c["d"], c["k"], c["n_epochs"], 5, 2
     if slot == "knn_tc_kernel (trust ranks)":             # the contraction over the tiles it visits
         return "tensor", 2.0 * n * n * d * fine_frac / world, "flop"
+    if slot == "knn_tc_kernel (trust coarse)":
+        # d >= 256: the coarse pass contracts a 122-dimensional principal projection of the rows
+        # (UMAP_TC_PROJ_K=58 one K slab, UMAP_TC_NO_PROJ the full-dimensional form)
+        kp = d
+        if d >= 256 and not os.environ.get("UMAP_TC_NO_PROJ"):
+            kp = 58 if int(os.environ.get("UMAP_TC_PROJ_K", "122")) <= 58 else 122
+        return "tensor", 2.0 * n * n * kp / world, "flop"
     if slot.startswith("knn_tc_kernel"):
         return "tensor", 2.0 * n * n * d / world, "flop"  # the n x n x d distance contraction, unpadded
     if slot == "sgd_kernel":                    # SURVEY 8(d) byte model
