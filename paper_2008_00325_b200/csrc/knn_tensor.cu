@@ -1526,11 +1526,42 @@ __global__ void row_tiles_kernel(const uint8_t* __restrict__ rowflags, int64_t r
     if (lane == 0) cnt[i] = c;
 }
 
-__global__ void regroup_keys_kernel(const int32_t* __restrict__ cnt, int64_t rows, int cut, uint32_t* __restrict__ keys,
-                                    int32_t* __restrict__ vals)
+// histogram of the rows' tile counts (0..nt), privatised in shared memory
+__global__ void tile_hist_kernel(const int32_t* __restrict__ cnt, int64_t rows, int nt, int32_t* __restrict__ hist)
+{
+    extern __shared__ int32_t hs[];
+    for (int v = threadIdx.x; v <= nt; v += blockDim.x) hs[v] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hs[min(cnt[i], nt)], 1);
+    __syncthreads();
+    for (int v = threadIdx.x; v <= nt; v += blockDim.x)
+        if (hs[v]) atomicAdd(&hist[v], hs[v]);
+}
+
+// out[0] = the regroup cut max(8, 2 median) (median = the element of rank rows / 2, as
+// std::nth_element), out[1] = rows above the cut; one thread
+__global__ void regroup_cut_kernel(const int32_t* __restrict__ hist, int nt, int64_t rows, int32_t* __restrict__ out)
+{
+    int64_t cum = 0;
+    int med = nt;
+    for (int v = 0; v <= nt; ++v) {
+        cum += hist[v];
+        if (cum > rows / 2) { med = v; break; }
+    }
+    const int cut = max(8, 2 * med);
+    int64_t above = 0;
+    for (int v = cut + 1; v <= nt; ++v) above += hist[v];
+    out[0] = cut;
+    out[1] = (int32_t)above;
+}
+
+__global__ void regroup_keys_kernel(const int32_t* __restrict__ cnt, int64_t rows, const int32_t* __restrict__ cutp,
+                                    uint32_t* __restrict__ keys, int32_t* __restrict__ vals)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows) return;
+    const int cut = *cutp;
     keys[i] = (cnt[i] > cut ? 0x80000000u : 0u) | (uint32_t)i;
     vals[i] = (int32_t)i;
 }
@@ -1549,9 +1580,15 @@ __global__ void block_flags_kernel(const uint8_t* __restrict__ rowflags, const i
     const int64_t b = blockIdx.x;
     const int64_t r0 = b * 256, r1 = r0 + 256 < rows ? r0 + 256 : rows;
     for (int t = threadIdx.x; t < nt; t += blockDim.x) {
-        uint8_t f = 0;
-        for (int64_t r = r0; r < r1 && !f; ++r) f = rowflags[(int64_t)pos2[r] * nt + t];
-        flags[b * nt + t] = f;
+        // OR over the block's rows, 16 independent loads in flight (an early-exit loop was one
+        // dependent L2 round trip per row: 0.145 ms at C2)
+        uint32_t f = 0;
+        for (int64_t r = r0; r < r1; r += 16) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (r + u < r1) f |= rowflags[(int64_t)pos2[r + u] * nt + t];
+        }
+        flags[b * nt + t] = f ? 1 : 0;
     }
 }
 
@@ -1731,7 +1768,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     // reference tiles where some row of a 256-row block may reach its largest threshold; the
     // split-precision pass then visits only those tiles (the others are certainly above every
     // threshold of every row of the block and add nothing to any count)
-    Scratch flags, tl, tcnt, rowfl, rcnt, rkeys, pos2, qperm2;
+    Scratch flags, tl, tcnt, rowfl, rcnt, rkeys, pos2, qperm2, rhist, rcut;
     const int64_t nqb = (qblocks + 1) / 2, ntl = (n + TC_BN - 1) / TC_BN;
     g_last_regrouped = 0;
     if (ordered && !getenv("UMAP_TC_NO_COARSE")) {
@@ -1833,20 +1870,22 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             UMAP_TRY(rcnt.alloc(sizeof(int32_t) * (size_t)rows, s));
             row_tiles_kernel<<<ceil_div(rows, 8), 256, 0, s>>>(rowfl.as<uint8_t>(), rows, (int)ntl, rcnt.as<int32_t>());
             UMAP_LAUNCH_CHECK("row_tiles_kernel");
-            std::vector<int32_t> hc((size_t)rows);
-            UMAP_CUDA_TRY(cudaMemcpyAsync(hc.data(), rcnt.p, sizeof(int32_t) * (size_t)rows, cudaMemcpyDeviceToHost, s));
-            UMAP_CUDA_TRY(cudaStreamSynchronize(s));
-            std::vector<int32_t> sorted_c = hc;
-            std::nth_element(sorted_c.begin(), sorted_c.begin() + rows / 2, sorted_c.end());
-            const int cut = std::max(8, 2 * sorted_c[(size_t)(rows / 2)]);
-            int64_t n_out = 0;
-            for (int32_t c : hc) n_out += c > cut;
-            g_last_regrouped = n_out;
-            if (n_out > 0) {
+            // the cut (twice the median tile count) on the device: no host round trip; the
+            // regroup kernels always run (with no row above the cut the order is unchanged)
+            UMAP_TRY(rhist.alloc(sizeof(int32_t) * (size_t)(ntl + 1), s));
+            UMAP_TRY(rcut.alloc(sizeof(int32_t) * 2, s));
+            UMAP_CUDA_TRY(cudaMemsetAsync(rhist.p, 0, sizeof(int32_t) * (size_t)(ntl + 1), s));
+            tile_hist_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows, 256), 4 * num_sms()), 256,
+                               sizeof(int32_t) * (size_t)(ntl + 1), s>>>(rcnt.as<int32_t>(), rows, (int)ntl,
+                                                                         rhist.as<int32_t>());
+            UMAP_LAUNCH_CHECK("tile_hist_kernel");
+            regroup_cut_kernel<<<1, 1, 0, s>>>(rhist.as<int32_t>(), (int)ntl, rows, rcut.as<int32_t>());
+            UMAP_LAUNCH_CHECK("regroup_cut_kernel");
+            {
                 UMAP_TRY(rkeys.alloc(sizeof(uint32_t) * (size_t)rows, s));
                 UMAP_TRY(pos2.alloc(sizeof(int32_t) * (size_t)rows, s));
                 UMAP_TRY(qperm2.alloc(sizeof(int32_t) * (size_t)rows, s));
-                regroup_keys_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(rcnt.as<int32_t>(), rows, cut,
+                regroup_keys_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(rcnt.as<int32_t>(), rows, rcut.as<int32_t>(),
                                                                        rkeys.as<uint32_t>(), pos2.as<int32_t>());
                 UMAP_LAUNCH_CHECK("regroup_keys_kernel");
                 UMAP_TRY(sort_pairs_u32(rkeys.as<uint32_t>(), pos2.as<int32_t>(), rows, s));
@@ -1883,8 +1922,11 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         // chunk the tile lists: a CTA pair walks at most CH tiles, so the block of regrouped rows
         // (most tiles) is spread over several pairs instead of being the launch's long pole
         std::vector<int32_t> cn((size_t)nqb);
+        int32_t cut_h[2] = {0, 0};
+        if (regroup) UMAP_CUDA_TRY(cudaMemcpyAsync(cut_h, rcut.p, sizeof(cut_h), cudaMemcpyDeviceToHost, s));
         UMAP_CUDA_TRY(cudaMemcpyAsync(cn.data(), tcnt.p, sizeof(int32_t) * nqb, cudaMemcpyDeviceToHost, s));
         UMAP_CUDA_TRY(cudaStreamSynchronize(s));
+        if (regroup) g_last_regrouped = cut_h[1];
         int CH = 32;
         if (const char* e = getenv("UMAP_TC_CHUNK")) CH = std::max(1, atoi(e));  // tuning knob
         int maxc = 0;

@@ -39,120 +39,144 @@ __global__ void pca_init_kernel(float* __restrict__ V, int d, int K)
     V[i] = (i & 127) < K ? (float)(r.x >> 8) * (1.0f / 8388608.0f) - 1.0f : 0.0f;
 }
 
-// G = W^T W (K x K, fp64), W d x K fp32 in rows of 128 (four partial sums per thread)
-__global__ void gram64_kernel(const float* __restrict__ W, int d, int K, double* __restrict__ G)
+// G = W^T W split over the rows of W: part[z][i][j] = sum over rows f = z, z + nz, ... (fp64),
+// then summed in a fixed order (gram_sum_kernel): deterministic, and nz x more CTAs than one
+// K x K grid walking all d rows (latency-bound: 84 us at d = 784)
+__global__ void gram64_part_kernel(const float* __restrict__ W, int d, int K, int nz, double* __restrict__ part)
 {
-    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x, z = blockIdx.z;
     if (j >= K) return;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int f = 0;
-    for (; f + 4 <= d; f += 4) {
+    double a0 = 0.0, a1 = 0.0;
+    int f = z;
+    for (; f + nz < d; f += 2 * nz) {
         a0 += (double)W[(int64_t)f * 128 + i] * (double)W[(int64_t)f * 128 + j];
-        a1 += (double)W[(int64_t)(f + 1) * 128 + i] * (double)W[(int64_t)(f + 1) * 128 + j];
-        a2 += (double)W[(int64_t)(f + 2) * 128 + i] * (double)W[(int64_t)(f + 2) * 128 + j];
-        a3 += (double)W[(int64_t)(f + 3) * 128 + i] * (double)W[(int64_t)(f + 3) * 128 + j];
+        a1 += (double)W[(int64_t)(f + nz) * 128 + i] * (double)W[(int64_t)(f + nz) * 128 + j];
     }
-    for (; f < d; ++f) a0 += (double)W[(int64_t)f * 128 + i] * (double)W[(int64_t)f * 128 + j];
-    G[i * K + j] = (a0 + a1) + (a2 + a3);
+    if (f < d) a0 += (double)W[(int64_t)f * 128 + i] * (double)W[(int64_t)f * 128 + j];
+    part[((int64_t)z * K + i) * K + j] = a0 + a1;
+}
+__global__ void gram_sum_kernel(const double* __restrict__ part, int nz, int K, double* __restrict__ G)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= K * K) return;
+    double g = 0.0;
+    for (int z = 0; z < nz; ++z) g += part[(int64_t)z * K * K + t];
+    G[t] = g;
+}
+// err2 = sum_{i,j} (G_ij - delta_ij)^2, one CTA, fixed-order tree reduction
+__global__ void orth_err_from_gram_kernel(const double* __restrict__ G, int K, double* __restrict__ err2)
+{
+    __shared__ double red[256];
+    double e = 0.0;
+    for (int t = threadIdx.x; t < K * K; t += blockDim.x) {
+        const double v = G[t] - ((t / K) == (t % K) ? 1.0 : 0.0);
+        e += v * v;
+    }
+    red[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *err2 = red[0];
 }
 
-// One CTA of 128 threads (K <= 128): G + jitter = L L^T (left-looking Cholesky, thread i owns row i
-// of L, stored column-major so that the lanes of a dot product read consecutive words; one
-// barrier per column), then Linv = L^-1 in place (columns right to left), written as B = Linv^T in
-// rows of 128 (B[j][k] = Linv[k][j], zero past K) so that V = W B is one tgemm128.
-// ok = 0 when a pivot is not positive.
-__global__ void __launch_bounds__(128) chol_kernel(const double* __restrict__ G, int K, float* __restrict__ Bt,
-                                                   int* __restrict__ ok)
+// Right-looking Cholesky of G (K x K, fp64, symmetric) in one CTA: G + jitter I = L L^T, L (lower,
+// row-major, K x K) to Lout.  Per column j: the pivot, the column scaled, then the rank-1 update of
+// the trailing triangle spread over the whole CTA (independent FMAs; the left-looking form's
+// per-row dot products were one dependent chain per thread: 0.34 ms at K = 122).  ok = 0 when a
+// pivot is not positive.
+__global__ void __launch_bounds__(512) chol_rl_kernel(const double* __restrict__ G, int K, double* __restrict__ Lout,
+                                                      int* __restrict__ ok)
 {
-    extern __shared__ double Lc[];  // L[i][m] at Lc[m * K + i]; then X = L^-1 in place
-    const int i = threadIdx.x;
-    for (int t = i; t < K * K; t += blockDim.x) Lc[(t % K) * K + t / K] = G[t];  // G symmetric: any layout
+    extern __shared__ double A[];  // A[r * K + c]
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int t = tid; t < K * K; t += nt) A[t] = G[t];
     __syncthreads();
     __shared__ double jitter;
-    if (i == 0) {
+    if (tid == 0) {
         double m = 0.0;
-        for (int t = 0; t < K; ++t) m = fmax(m, Lc[t * K + t]);
+        for (int t = 0; t < K; ++t) m = fmax(m, A[t * K + t]);
         jitter = 1e-12 * m;
     }
-    __syncthreads();
-    auto dot = [&](int r1, int r2, int len) {  // sum_{m < len} L[r1][m] L[r2][m]
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int m = 0;
-        for (; m + 4 <= len; m += 4) {
-            a0 += Lc[m * K + r1] * Lc[m * K + r2];
-            a1 += Lc[(m + 1) * K + r1] * Lc[(m + 1) * K + r2];
-            a2 += Lc[(m + 2) * K + r1] * Lc[(m + 2) * K + r2];
-            a3 += Lc[(m + 3) * K + r1] * Lc[(m + 3) * K + r2];
-        }
-        for (; m < len; ++m) a0 += Lc[m * K + r1] * Lc[m * K + r2];
-        return (a0 + a1) + (a2 + a3);
-    };
     for (int j = 0; j < K; ++j) {
-        if (i == j) {
-            const double sdiag = Lc[j * K + j] + jitter - dot(j, j, j);
-            if (!(sdiag > 0.0)) *ok = 0;
-            Lc[j * K + j] = sqrt(fmax(sdiag, 1e-300));
+        __syncthreads();
+        if (tid == 0) {
+            const double dj = A[j * K + j] + jitter;
+            if (!(dj > 0.0)) *ok = 0;
+            A[j * K + j] = sqrt(fmax(dj, 1e-300));
         }
         __syncthreads();
-        if (i > j && i < K) Lc[j * K + i] = (Lc[j * K + i] - dot(i, j, j)) / Lc[j * K + j];
-    }
-    __syncthreads();
-    // X = L^-1 in place, columns right to left: X[j][j] = 1 / L[j][j],
-    // X[i][j] = -(sum_{m=j+1}^{i} X[i][m] L[m][j]) / L[j][j] for i > j (row i of X right of j is done,
-    // column j of L is still intact until the barrier)
-    for (int j = K - 1; j >= 0; --j) {
-        double x = 0.0;
-        const double ljj = Lc[j * K + j];
-        if (i > j && i < K) {
-            double a0 = 0.0, a1 = 0.0;
-            int m = j + 1;
-            for (; m + 2 <= i + 1; m += 2) {
-                a0 += Lc[m * K + i] * Lc[j * K + m];
-                a1 += Lc[(m + 1) * K + i] * Lc[j * K + m + 1];
-            }
-            if (m <= i) a0 += Lc[m * K + i] * Lc[j * K + m];
-            x = -(a0 + a1) / ljj;
+        const double inv = 1.0 / A[j * K + j];
+        for (int r = j + 1 + tid; r < K; r += nt) A[r * K + j] *= inv;
+        __syncthreads();
+        // trailing lower triangle: warp w takes rows j+1+w, j+1+w+NW, ..., lane l columns
+        // j+1+l, j+1+l+32, ... <= r (no index division)
+        const int lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+        for (int r = j + 1 + w; r < K; r += nw) {
+            const double lr = A[r * K + j];
+            for (int c = j + 1 + lane; c <= r; c += 32) A[r * K + c] -= lr * A[c * K + j];
         }
-        __syncthreads();
-        if (i > j && i < K) Lc[j * K + i] = x;
-        if (i == j) Lc[j * K + j] = 1.0 / ljj;
-        __syncthreads();
     }
     __syncthreads();
-    // Bt[j][k] = X[k][j] (k >= j; X[k][j] at Lc[j * K + k]), rows of 128
-    for (int t = i; t < K * 128; t += blockDim.x) {
-        const int j = t / 128, k = t % 128;
-        Bt[t] = (k < K && k >= j) ? (float)Lc[j * K + k] : 0.0f;
+    for (int t = tid; t < K * K; t += nt) {
+        const int r = t / K, c = t % K;
+        Lout[t] = c <= r ? A[t] : 0.0;
     }
 }
 
-// err2 += sum_{i,j} ((P^T P)_ij - delta_ij)^2 (fp64, P the fp32 basis as used)
-__global__ void orth_err_kernel(const float* __restrict__ P, int d, int K, double* __restrict__ err2)
+// V = W L^-T (d x 128 fp32, columns >= K zero): row w of W solves L v^T = w^T by forward
+// substitution, one warp per row (lane l holds v_m for m = l mod 32), L broadcast from shared memory
+__global__ void __launch_bounds__(256) trsm_rows_kernel(const float* __restrict__ W, int d, int K,
+                                                        const double* __restrict__ L, float* __restrict__ V)
 {
-    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= K) return;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int f = 0;
-    for (; f + 4 <= d; f += 4) {
-        a0 += (double)P[(int64_t)f * 128 + i] * (double)P[(int64_t)f * 128 + j];
-        a1 += (double)P[(int64_t)(f + 1) * 128 + i] * (double)P[(int64_t)(f + 1) * 128 + j];
-        a2 += (double)P[(int64_t)(f + 2) * 128 + i] * (double)P[(int64_t)(f + 2) * 128 + j];
-        a3 += (double)P[(int64_t)(f + 3) * 128 + i] * (double)P[(int64_t)(f + 3) * 128 + j];
+    extern __shared__ double Ls[];
+    for (int t = threadIdx.x; t < K * K; t += blockDim.x) Ls[t] = L[t];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= d) return;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};  // v[q] = v_{lane + 32 q}
+    for (int i = 0; i < K; ++i) {
+        double part = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = lane + 32 * q;
+            if (m < i) part += Ls[i * K + m] * v[q];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        const double vi = ((double)W[(int64_t)row * 128 + i] - part) / Ls[i * K + i];
+        if ((i & 31) == lane) v[i >> 5] = vi;
     }
-    for (; f < d; ++f) a0 += (double)P[(int64_t)f * 128 + i] * (double)P[(int64_t)f * 128 + j];
-    const double e = ((a0 + a1) + (a2 + a3)) - (i == j ? 1.0 : 0.0);
-    atomicAdd(err2, e * e);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int m = lane + 32 * q;
+        V[(int64_t)row * 128 + m] = m < K ? (float)v[q] : 0.0f;
+    }
+}
+
+constexpr int GRAM_NZ = 16;
+umap_status gram64(const float* W, int d, int K, double* G, cudaStream_t s)
+{
+    Scratch part;
+    UMAP_TRY(part.alloc(sizeof(double) * (size_t)GRAM_NZ * K * K, s));
+    gram64_part_kernel<<<dim3((unsigned)ceil_div(K, 128), (unsigned)K, GRAM_NZ), 128, 0, s>>>(W, d, K, GRAM_NZ,
+                                                                                              part.as<double>());
+    UMAP_LAUNCH_CHECK("gram64_part_kernel");
+    gram_sum_kernel<<<ceil_div(K * K, 256), 256, 0, s>>>(part.as<double>(), GRAM_NZ, K, G);
+    UMAP_LAUNCH_CHECK("gram_sum_kernel");
+    return UMAP_OK;
 }
 
 // CholeskyQR: V = W L^-T with W^T W = L L^T (W, V: d x 128, columns >= K zero)
-umap_status cholqr(const float* W, float* V, int d, int K, double* G, float* Bt, int* ok, cudaStream_t s)
+umap_status cholqr(const float* W, float* V, int d, int K, double* G, double* L, int* ok, cudaStream_t s)
 {
-    gram64_kernel<<<dim3((unsigned)ceil_div(K, 128), (unsigned)K), 128, 0, s>>>(W, d, K, G);
-    UMAP_LAUNCH_CHECK("gram64_kernel");
-    chol_kernel<<<1, 128, sizeof(double) * (size_t)K * K, s>>>(G, K, Bt, ok);
-    UMAP_LAUNCH_CHECK("chol_kernel");
-    tgemm128_kernel<false><<<(unsigned)ceil_div(d, 128), 256, 0, s>>>(W, d, 1, 128, 128, nullptr, 0.0, Bt, V);
-    UMAP_LAUNCH_CHECK("tgemm128_kernel");
+    UMAP_TRY(gram64(W, d, K, G, s));
+    chol_rl_kernel<<<1, 512, sizeof(double) * (size_t)K * K, s>>>(G, K, L, ok);
+    UMAP_LAUNCH_CHECK("chol_rl_kernel");
+    trsm_rows_kernel<<<(unsigned)ceil_div(d, 8), 256, sizeof(double) * (size_t)K * K, s>>>(W, d, K, L, V);
+    UMAP_LAUNCH_CHECK("trsm_rows_kernel");
     return UMAP_OK;
 }
 
@@ -181,12 +205,13 @@ umap_status pca_basis(const float* X, int64_t n, int d, const double* colsum, in
     UMAP_TRY(w.alloc(sizeof(float) * (size_t)d * 128, s));
     UMAP_TRY(xs.alloc(sizeof(float) * (size_t)S * d, s));
     UMAP_TRY(g.alloc(sizeof(double) * (size_t)K * K, s));
-    UMAP_TRY(l.alloc(sizeof(float) * (size_t)128 * 128, s));
+    UMAP_TRY(l.alloc(sizeof(double) * (size_t)K * K, s));
     UMAP_TRY(okb.alloc(sizeof(int), s));
     UMAP_TRY(err.alloc(sizeof(double), s));
     static PerDeviceOnce attr;
     if (attr.first()) {
-        UMAP_CUDA_TRY(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(chol_rl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
+        UMAP_CUDA_TRY(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
     }
     const int one = 1;
     UMAP_CUDA_TRY(cudaMemcpyAsync(okb.p, &one, sizeof(int), cudaMemcpyHostToDevice, s));
@@ -210,9 +235,11 @@ umap_status pca_basis(const float* X, int64_t n, int d, const double* colsum, in
     split_sum_kernel<<<(unsigned)ceil_div((int64_t)d * 128, 256), 256, 0, s>>>(wp.as<float>(), KSPLIT, (int64_t)d * 128,
                                                                               w.as<float>());
     UMAP_LAUNCH_CHECK("split_sum_kernel");
-    UMAP_TRY(cholqr(w.as<float>(), P, d, K, g.as<double>(), l.as<float>(), okb.as<int>(), s));
-    orth_err_kernel<<<dim3((unsigned)ceil_div(K, 128), (unsigned)K), 128, 0, s>>>(P, d, K, err.as<double>());
-    UMAP_LAUNCH_CHECK("orth_err_kernel");
+    UMAP_TRY(cholqr(w.as<float>(), P, d, K, g.as<double>(), l.as<double>(), okb.as<int>(), s));
+    // ||P^T P - I||_F^2 of the fp32 basis as used (fp64 Gram, fixed-order sums)
+    UMAP_TRY(gram64(P, d, K, g.as<double>(), s));
+    orth_err_from_gram_kernel<<<1, 256, 0, s>>>(g.as<double>(), K, err.as<double>());
+    UMAP_LAUNCH_CHECK("orth_err_from_gram_kernel");
     sigma_kernel<<<1, 1, 0, s>>>(err.as<double>(), okb.as<int>(), sigma);
     UMAP_LAUNCH_CHECK("sigma_kernel");
     return UMAP_OK;
