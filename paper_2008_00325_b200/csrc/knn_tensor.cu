@@ -626,6 +626,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 tmem_ld32(taddr + c, v);
                 const int64_t jb = rb + c;
                 const int valid_cols = (int)imin64(32, r_hi - jb);
+                // out-of-range columns (zero-filled TMA rows: accumulator 0) never flag
+                if (valid_cols < 32) {
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) v[u] = u < valid_cols ? v[u] : -INFINITY;
+                }
                 float rmax;
                 if (a.chunk_rmax) {
                     rmax = __ldg(a.chunk_rmax + (jb >> 5));
@@ -648,11 +653,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     lim = s * s * 1.000001f;
                 }
                 const float vlim = -0.5f * (lim + a.margin * (qn + rmax));
-                uint32_t cm = 0;
+                // the tile is flagged for the row when any column reaches vlim: a max tree
+                // (FMNMX3) instead of a 32-bit column mask
+                float m16[16];
 #pragma unroll
-                for (int u = 0; u < 32; ++u) cm |= (uint32_t)(v[u] >= vlim) << u;
-                if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
-                hit |= valid && cm != 0;
+                for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+                for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+                    for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
+                }
+                hit |= valid && m16[0] >= vlim;
             }
             tc_fence_before();
             __syncwarp();
