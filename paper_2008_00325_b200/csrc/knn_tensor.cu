@@ -619,17 +619,24 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             const int tile = tile_at(t);
             const int64_t rb = r_lo + (int64_t)tile * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
+            // the thread's 128 columns as four 32-column chunks: all four TMEM loads in flight
+            // before one wait, four independent max trees (FMNMX3); the tile is flagged for the
+            // row when some column reaches its chunk's limit
+            constexpr int NCH = TC_BN / 2 / 32;
+            float v[NCH][32];
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) tmem_ld32_nw(taddr + half * (TC_BN / 2) + 32 * h, v[h]);
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) tmem_ld_wait(v[h]);
             bool hit = false;
-#pragma unroll 1
-            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2); c += 32) {
-                float v[32];
-                tmem_ld32(taddr + c, v);
-                const int64_t jb = rb + c;
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) {
+                const int64_t jb = rb + half * (TC_BN / 2) + 32 * h;
                 const int valid_cols = (int)imin64(32, r_hi - jb);
                 // out-of-range columns (zero-filled TMA rows: accumulator 0) never flag
                 if (valid_cols < 32) {
 #pragma unroll
-                    for (int u = 0; u < 32; ++u) v[u] = u < valid_cols ? v[u] : -INFINITY;
+                    for (int u = 0; u < 32; ++u) v[h][u] = u < valid_cols ? v[h][u] : -INFINITY;
                 }
                 float rmax;
                 if (a.chunk_rmax) {
@@ -649,15 +656,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
 #pragma unroll
                         for (int o = 16; o; o >>= 1) br = fmaxf(br, __shfl_xor_sync(0xffffffffu, br, o));
                     }
-                    const float s = aq + br;
-                    lim = s * s * 1.000001f;
+                    const float sb = aq + br;
+                    lim = sb * sb * 1.000001f;
                 }
                 const float vlim = -0.5f * (lim + a.margin * (qn + rmax));
-                // the tile is flagged for the row when any column reaches vlim: a max tree
-                // (FMNMX3) instead of a 32-bit column mask
                 float m16[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+                for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[h][2 * i], v[h][2 * i + 1]);
 #pragma unroll
                 for (int w = 8; w >= 1; w >>= 1) {
 #pragma unroll
