@@ -12,7 +12,7 @@ namespace {
 // reduction over the sample).  128 x 128 outputs per CTA, 256 threads with 8 x 8 each, the
 // reduction staged in slabs of 16.
 template <bool TRANS_A>
-__global__ void __launch_bounds__(256) tgemm128_kernel(const float* __restrict__ A, int64_t M, int64_t stride,
+__global__ void __launch_bounds__(256, 2) tgemm128_kernel(const float* __restrict__ A, int64_t M, int64_t stride,
                                                        int64_t kdim, int lda, const double* __restrict__ colsum,
                                                        double inv_n, const float* __restrict__ B,
                                                        float* __restrict__ C)
@@ -34,23 +34,30 @@ __global__ void __launch_bounds__(256) tgemm128_kernel(const float* __restrict__
     // each thread stages 8 A and 8 B values per slab; the next slab is loaded into registers
     // while the current one is multiplied
     float ra[8], rb[8];
+    // per-thread bases: (non-TRANS) A rows r0 + tid / 16 + 16 q, column k0 + tid % 16 (the column
+    // mean loaded once per slab); (TRANS) A[k0 + tid / 128 + 2 q][r0 + tid % 128]; B[k0 + tid / 128 + 2 q][tid % 128]
+    const int64_t a_row = TRANS_A ? r0 + (tid & 127) : r0 + (tid >> 4);
+    const int a_k = TRANS_A ? (tid >> 7) : (tid & 15);
+    const float* pa = TRANS_A ? A + a_row : A + a_row * stride * lda + a_k;
+    const int64_t a_step = TRANS_A ? 2 * (int64_t)lda : 16 * stride * (int64_t)lda;  // per q
+    const float* pb = B + (tid >> 7) * 128 + (tid & 127);
     auto load = [&](int64_t k0) {
+        if (TRANS_A) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int i = tid + 256 * q;
-            if (TRANS_A) {  // A(r, k) = Xs[k][r]: coalesced over r
-                const int kk = i >> 7, rr = i & 127;
-                const int64_t r = r0 + rr, k = k0 + kk;
-                ra[q] = (r < M && k < k_hi) ? A[k * lda + r] : 0.0f;
-            } else {        // A(r, k) = x[r stride][k] - mean_k: coalesced over k
-                const int rr = i >> 4, kk = i & 15;
-                const int64_t r = r0 + rr, k = k0 + kk;
-                ra[q] = (r < M && k < k_hi) ? A[r * stride * lda + k] - (colsum ? (float)(colsum[k] * inv_n) : 0.0f)
-                                            : 0.0f;
+            for (int q = 0; q < 8; ++q) {
+                const int64_t k = k0 + a_k + 2 * q;
+                ra[q] = (a_row < M && k < k_hi) ? pa[k * lda] : 0.0f;
             }
-            const int kb = i >> 7, c = i & 127;
-            rb[q] = (k0 + kb < k_hi) ? B[(k0 + kb) * 128 + c] : 0.0f;
+        } else {
+            const int64_t k = k0 + a_k;
+            const bool kv = k < k_hi;
+            const float mean = (kv && colsum) ? (float)(colsum[k] * inv_n) : 0.0f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                ra[q] = (kv && a_row + 16 * q < M) ? pa[q * a_step + k0] - mean : 0.0f;
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rb[q] = (k0 + (tid >> 7) + 2 * q < k_hi) ? pb[(k0 + 2 * q) * 128] : 0.0f;
     };
     auto store = [&]() {
 #pragma unroll
