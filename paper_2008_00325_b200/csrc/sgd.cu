@@ -441,7 +441,12 @@ __global__ void __launch_bounds__(1024, 1) sgd_flat3_kernel(SgdArgs A)
 // hl << 21 | t), so the per-epoch scan (A) reads shared memory instead of streaming 8 bytes per
 // record from L2 every epoch; the due lists hold 16-bit record indices.  Same edge work, batches
 // and fixed-point sums as flat3 (R13: Y is bit-identical).
-template <int DIM, int MC, int NT = 1024, int MINB = 1>
+// HOG: the Hogwild mode (R14) on the same structure: positions in place (Y0 == Y1), each due edge
+// reads the live head, tail and sample rows (L1-cached: staleness bounded to one epoch by the grid
+// barrier's acquire), moves its head through the attractive and the m repulsive updates in
+// registers and pushes -g_att to the tail and the head's total delta with fp32 vector atomics
+// (process_edge, as the persistent Hogwild kernel); no accumulators, no end-of-epoch vertex pass.
+template <int DIM, int MC, int NT = 1024, int MINB = 1, bool HOG = false>
 __global__ void __launch_bounds__(NT, MINB) sgd_flat5_kernel(SgdArgs A)
 {
     extern __shared__ __align__(16) unsigned char sgd_smem[];
@@ -513,12 +518,14 @@ __global__ void __launch_bounds__(NT, MINB) sgd_flat5_kernel(SgdArgs A)
         rr[i] = __int_as_float(rec.y);
         rx[i] = (uint32_t)rec.x;
     }
-    for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(A.Y0 + (int64_t)v_lo * DIM + i);
-    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    if (!HOG) {
+        for (int i = threadIdx.x; i < np * DIM; i += blockDim.x) yhead[i] = __ldcg(A.Y0 + (int64_t)v_lo * DIM + i);
+        for (int i = threadIdx.x; i < np; i += blockDim.x) {
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) {
-            if (wide) acc64[c * vt + i] = 0ull;
-            else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+            for (int c = 0; c < DIM; ++c) {
+                if (wide) acc64[c * vt + i] = 0ull;
+                else { acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0; }
+            }
         }
     }
     if (threadIdx.x == 0) { s_step = 0; s_cur[0] = 0; s_cur[1] = 0; }
@@ -538,30 +545,37 @@ __global__ void __launch_bounds__(NT, MINB) sgd_flat5_kernel(SgdArgs A)
         const int nl = s_nlist;
         const int nb = (nl + 31) >> 5;
         // static strided batches (flat3): warp w takes batches w, w + NT / 32, ...
+        const float alpha = HOG ? __fmul_rn(A.alpha0, __fsub_rn(1.0f, __fdiv_rn((float)epoch, (float)A.n_epochs))) : 0.0f;
         for (int b = warp; b < nb; b += NT / 32) {
             const int j = b + lane * nb;
             const bool act = j < nl;
             const uint32_t ent = act ? rx[list[j]] : 0u;
             const int hl = (int)(ent >> 21), t = act ? (int)(ent & 0x1FFFFFu) : v_lo;
             int qa[DIM];
-            edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, hl, t, act, qa);
-            if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
+            if constexpr (HOG) {
+                if (act) process_edge<DIM, false, MC, true>(A, Yr, Yw, epoch, alpha, v_lo + hl, t, qa);
+            } else {
+                edge_terms<DIM, MC>(A, Yr, epoch, nn, K, yhead, v_lo, hl, t, act, qa);
+                if (act) acc_add<DIM>(acc_lo, acc_hi, acc64, vt, hl, wide, qa);
+            }
         }
         if (epoch + 1 < A.e_end) scan(epoch + 1, buf ^ 1, split);
         __syncthreads();
-        for (int i = threadIdx.x; i < np; i += blockDim.x) {
-            const int v = v_lo + i;
+        if (!HOG) {
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                const int v = v_lo + i;
 #pragma unroll
-            for (int c = 0; c < DIM; ++c) {
-                long long tot;
-                if (wide) { tot = (long long)acc64[c * vt + i]; acc64[c * vt + i] = 0ull; }
-                else {
-                    tot = (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
-                    acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0;
+                for (int c = 0; c < DIM; ++c) {
+                    long long tot;
+                    if (wide) { tot = (long long)acc64[c * vt + i]; acc64[c * vt + i] = 0ull; }
+                    else {
+                        tot = (long long)acc_hi[c * vt + i] * 65536LL + (long long)acc_lo[c * vt + i];
+                        acc_lo[c * vt + i] = 0u; acc_hi[c * vt + i] = 0;
+                    }
+                    const float y = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
+                    yhead[i * DIM + c] = y;
+                    Yw[(int64_t)v * DIM + c] = y;
                 }
-                const float y = (float)((double)yhead[i * DIM + c] + (double)tot * (1.0 / 16777216.0));
-                yhead[i * DIM + c] = y;
-                Yw[(int64_t)v * DIM + c] = y;
             }
         }
         if (epoch + 1 < A.e_end) {
@@ -966,7 +980,7 @@ bool sgd_sched_enabled() { return sgd_sched_mode() == 1; }
 // ver: 1 = the round-1 flat kernel, 2 = flat2, 3 = flat3 when every CTA range fits one piece
 // (else flat2)
 template <int DIM, int MC>
-umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver, int cps_req, bool* retry)
+umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver, int cps_req, bool* retry, bool hog = false)
 {
     // one CTA of 32 warps per SM, or (flat5, cps_req = 2, the default) two CTAs of 18 warps per SM:
     // 36 warps at <= 56 registers carry 1152 due edges per round instead of 1024 (C2: ~3,090 due
@@ -1148,10 +1162,11 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver, int
         if (smem5 <= 200 * 1024 && A.list_cap <= 65535) {
             smem = smem5;
             ver = 5;
-            kern = cps == 2 ? sgd_flat5_kernel<DIM, MC, 576, 2> : sgd_flat5_kernel<DIM, MC>;
+            kern = hog ? (cps == 2 ? sgd_flat5_kernel<DIM, MC, 576, 2, true> : sgd_flat5_kernel<DIM, MC, 1024, 1, true>)
+                       : (cps == 2 ? sgd_flat5_kernel<DIM, MC, 576, 2> : sgd_flat5_kernel<DIM, MC>);
             nt = cps == 2 ? 576 : 1024;
-            static PerDeviceOnce attr5[2];
-            if (attr5[cps - 1].first())
+            static PerDeviceOnce attr5[4];
+            if (attr5[(cps - 1) + (hog ? 2 : 0)].first())
                 UMAP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             // carveout: the smallest shared-memory share that holds cps CTAs (the rest is L1, which
             // caches the gathered positions); set per launch (the size depends on the graph)
@@ -1167,9 +1182,9 @@ umap_status launch_sgd_flat(SgdArgs A, int64_t nnz, cudaStream_t s, int ver, int
             }
         }
     }
-    if (cps != 1 && ver != 5) {
+    if ((cps != 1 || hog) && ver != 5) {
         if (retry) *retry = true;
-        set_last_error("two CTAs per SM need the flat5 kernel");
+        set_last_error(hog ? "the flat Hogwild form needs the flat5 layout" : "two CTAs per SM need the flat5 kernel");
         return UMAP_ERR_CUDA;
     }
     void* args[] = {&A};
@@ -1206,6 +1221,19 @@ umap_status launch_sgd(const SgdArgs& A, bool det, cudaStream_t s)
                 st = A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, ver, 1, nullptr)
                               : launch_sgd_flat<DIM, 0>(A, A.nnz, s, ver, 1, nullptr);
             return st;
+        }
+        // Hogwild on flat5's structure (default; tuning knob UMAP_SGD_HOG_CHUNK=1: the persistent
+        // chunk kernel), falling back to the chunk kernel when the flat5 layout does not fit
+        if (!det && (sv == 0) && sgd_sched_mode() == 2 && !getenv("UMAP_SGD_HOG_CHUNK")) {
+            bool retry = false;
+            umap_status st = A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, 3, 2, &retry, true)
+                                      : launch_sgd_flat<DIM, 0>(A, A.nnz, s, 3, 2, &retry, true);
+            if (st != UMAP_OK && retry) {
+                retry = false;
+                st = A.m == 5 ? launch_sgd_flat<DIM, 5>(A, A.nnz, s, 3, 1, &retry, true)
+                              : launch_sgd_flat<DIM, 0>(A, A.nnz, s, 3, 1, &retry, true);
+            }
+            if (st == UMAP_OK || !retry) return st;
         }
     }
     return launch_sgd_persistent<DIM>(A, det, s);
