@@ -220,24 +220,39 @@ struct DevOut {
     }
 };
 
+// Stage timer without host synchronisation: lap(&field) records an event on the stream and
+// remembers where its milliseconds go; resolve() (after the call's final stream synchronisation)
+// writes every lap's device time and returns their sum.  (A synchronising lap left the GPU idle
+// at every stage boundary while the host enqueued the next stage.)
 struct Timer {
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaStream_t s;
-    explicit Timer(cudaStream_t st) : s(st)
+    std::vector<cudaEvent_t> ev;
+    std::vector<double*> dst;
+    explicit Timer(cudaStream_t st) : s(st) { mark(nullptr); }
+    ~Timer()
     {
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, s);
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
     }
-    ~Timer() { cudaEventDestroy(e0); cudaEventDestroy(e1); }
-    double lap()
+    void mark(double* d)
     {
-        cudaEventRecord(e1, s);
-        cudaEventSynchronize(e1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        std::swap(e0, e1);
-        return ms;
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+        dst.push_back(d);
+    }
+    void lap(double* d) { mark(d); }
+    double resolve()
+    {
+        double tot = 0.0;
+        for (size_t i = 1; i < ev.size(); ++i) {
+            float ms = 0.f;
+            cudaEventSynchronize(ev[i]);
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            if (dst[i]) *dst[i] = ms;
+            tot += ms;
+        }
+        return tot;
     }
 };
 
@@ -650,7 +665,7 @@ umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const
     UMAP_TRY(acol.alloc(sizeof(int32_t) * (size_t)n * k, s));
     UMAP_TRY(aw.alloc(sizeof(float) * (size_t)n * k, s));
     UMAP_TRY(smooth_knn(dist, idx, n, k, nullptr, nullptr, aw.as<float>(), acol.as<int32_t>(), s));
-    st.ms_smooth = tm.lap();
+    tm.lap(&st.ms_smooth);
     // a5
     const int64_t cap = 2 * n * (int64_t)k;
     Scratch indptr, col, val;
@@ -674,18 +689,18 @@ umap_status fit_from_knn(const int32_t* idx, const float* dist, int64_t n, const
         g_col = scol.as<int32_t>();
         g_val = sval.as<float>();
     }
-    st.ms_union = tm.lap();
+    tm.lap(&st.ms_union);
     // a7 (random, R11, or spectral on the graph the SGD uses, R18)
     if (p.init == 1)
         UMAP_TRY(spectral_init(g_indptr, g_col, g_val, n, dim, p.seed, p.spectral_iters > 0 ? p.spectral_iters : 300,
                                Yd, s));
     else
         UMAP_TRY(random_init(n, dim, p.seed, Yd, s));
-    st.ms_init = tm.lap();
+    tm.lap(&st.ms_init);
     // a6 + a8
     int64_t positives = 0;
     UMAP_TRY(optimize_layout(g_indptr, g_col, g_val, n, nnz, Yd, &p, 1, p.n_epochs, &positives, s));
-    st.ms_sgd = tm.lap();
+    tm.lap(&st.ms_sgd);
     bool bad = false;
     UMAP_TRY(any_nonfinite(Yd, n * (int64_t)dim, &bad, s));
     if (bad) { set_last_error("embedding became non-finite"); return UMAP_ERR_NONFINITE_EMBEDDING; }
@@ -783,13 +798,13 @@ static umap_status fit_impl(const float* X, int64_t n, int32_t d, const int32_t*
     UMAP_TRY(any_nonfinite(Xd.p, n * (int64_t)d, &bad, s));
     if (bad) { set_last_error("X contains NaN or Inf"); return UMAP_ERR_NONFINITE_INPUT; }
     umap_fit_stats st{};
-    double t_pre = tm.lap();
+    tm.lap(nullptr);  // staging + input check
     // a2 kNN
     Scratch idx, dist;
     UMAP_TRY(idx.alloc(sizeof(int32_t) * (size_t)n * k, s));
     UMAP_TRY(dist.alloc(sizeof(float) * (size_t)n * k, s));
     UMAP_TRY(run_knn(&p, Xd.p, n, Xd.p, n, d, k, 0, 1, 0, 0, idx.as<int32_t>(), dist.as<float>(), s));
-    st.ms_knn = tm.lap();
+    tm.lap(&st.ms_knn);
     // labels on the device (staged if given in host memory)
     const int32_t* lab_d = labels;
     Scratch lab_buf;
@@ -805,12 +820,12 @@ static umap_status fit_impl(const float* X, int64_t n, int32_t d, const int32_t*
             return UMAP_ERR_K_OUT_OF_RANGE;
         }
         UMAP_TRY(trust_device(Xd.p, d, Yd.p, dim, n, p.trust_k, p.knn_mode, &st.trustworthiness, &st.trust_penalty, s));
-        st.ms_trust = tm.lap();
+        tm.lap(&st.ms_trust);
     }
     UMAP_TRY(Yd.finish(s));
+    tm.lap(nullptr);
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
-    double t_post = tm.lap();
-    st.ms_total = t_pre + st.ms_knn + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + st.ms_trust + t_post;
+    st.ms_total = tm.resolve();
     st.gpu_launches = (int32_t)(g_launches - launches0);
     if (stats) *stats = st;
     return UMAP_OK;
@@ -843,12 +858,12 @@ umap_status umap_fit_knn(const int32_t* knn_idx, const float* knn_dist, int64_t 
     DevOut Yd;
     UMAP_TRY(Yd.make(Y, (size_t)n * dim, s));
     umap_fit_stats st{};
-    double t_pre = tm.lap();
+    tm.lap(nullptr);
     UMAP_TRY(fit_from_knn(idx_d, dist_d.p, n, p, Yd.p, st, tm, s));
     UMAP_TRY(Yd.finish(s));
+    tm.lap(nullptr);
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
-    double t_post = tm.lap();
-    st.ms_total = t_pre + st.ms_smooth + st.ms_union + st.ms_init + st.ms_sgd + t_post;
+    st.ms_total = tm.resolve();
     st.gpu_launches = (int32_t)(g_launches - launches0);
     if (stats) *stats = st;
     return UMAP_OK;
