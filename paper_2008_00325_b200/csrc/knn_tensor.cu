@@ -1419,6 +1419,7 @@ static umap_status knn_tensor_impl(const float* Xq, int64_t nq, const float* Xr,
     const int64_t qblocks = (nq + TC_BM - 1) / TC_BM;
     int64_t splits = std::max<int64_t>(1, (num_sms() + qblocks - 1) / qblocks);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, nr / (4 * TC_BN)));
+    if (const char* e = getenv("UMAP_TC_KNN_SPLITS")) splits = std::max(1, atoi(e));  // tuning knob
     if (pivot_order) splits = 1;
     int64_t split_len = (nr + splits - 1) / splits;
     split_len = (split_len + TC_BN - 1) / TC_BN * TC_BN;
