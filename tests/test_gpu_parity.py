@@ -292,6 +292,45 @@ def test_sgd_flat_pieces_bitidentical(O, monkeypatch):
     assert np.abs(np_(Yg) - ref).max() <= 1e-4
 
 
+@pytest.mark.parametrize("dim,m", [(2, 5), (1, 5), (3, 3), (4, 7)])
+def test_sgd_deterministic_kernels_bitidentical(O, monkeypatch, dim, m):
+    """Every deterministic SGD form gives the same bytes (R13: per-term fixed point, integer sums):
+    flat5 as two CTAs per SM (the default) and as one, flat3 (records streamed from L2), flat4 (the
+    materialised schedule) and flat2 (pieces); the positives count is the schedule's."""
+    X, indptr, col, val = _graph(O, n=5000)
+    Y0 = cu(synth.uniform_embedding(5000, dim, seed=3))
+    outs, pos = [], []
+    for env in ({}, {"UMAP_SGD_CPS": "1"}, {"UMAP_SGD_SCHED": "0"}, {"UMAP_SGD_SCHED": "1"}, {"UMAP_SGD_VT": "64"}):
+        for kk in ("UMAP_SGD_CPS", "UMAP_SGD_SCHED", "UMAP_SGD_VT"):
+            monkeypatch.delenv(kk, raising=False)
+        for kk, vv in env.items():
+            monkeypatch.setenv(kk, vv)
+        Yg = Y0.clone()
+        pos.append(U.optimize(cu(indptr), cu(col), cu(val), Yg, e_begin=1, e_end=60, n_epochs=60, a=A_, b=B_,
+                              seed=11, negative_sample_rate=m))
+        outs.append(np_(Yg))
+    for kk in ("UMAP_SGD_CPS", "UMAP_SGD_SCHED", "UMAP_SGD_VT"):
+        monkeypatch.delenv(kk, raising=False)
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
+    assert len(set(pos)) == 1
+
+
+def test_hogwild_flat_and_chunk_kernels_vs_oracle(O, monkeypatch):
+    """Hogwild (R14) on flat5's structure (default) and on the persistent chunk kernel
+    (UMAP_SGD_HOG_CHUNK=1): both fits' trustworthiness within 0.005 of the oracle's own fit."""
+    c = synth.CONFIGS["C1"]
+    X = synth.lowrank(c["n"], c["d"], c["blobs"], c["seed"])
+    T_ref = O.trustworthiness(X, O.fit(X, k=15, n_epochs=200, a=A_, b=B_, seed=2, mode="hogwild"), 15)
+    for chunk in (False, True):
+        if chunk:
+            monkeypatch.setenv("UMAP_SGD_HOG_CHUNK", "1")
+        Y, st = U.fit(cu(X), n_neighbors=15, n_epochs=200, a=A_, b=B_, seed=2, sgd_mode="hogwild")
+        monkeypatch.delenv("UMAP_SGD_HOG_CHUNK", raising=False)
+        T, _ = U.trustworthiness(cu(X), Y, 15)
+        assert abs(T - T_ref) <= 0.005, (chunk, T, T_ref)
+
+
 def test_sgd_positive_count_matches_schedule(O):
     X, indptr, col, val = _graph(O, n=600)
     N = 50
