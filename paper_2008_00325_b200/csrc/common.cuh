@@ -49,7 +49,7 @@ struct ProfScope {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     ProfScope(int sl, cudaStream_t st) : slot(sl), s(st)
     {
-        if (profiling_enabled() && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
+        if (sl >= 0 && profiling_enabled() && cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess)
             cudaEventRecord(e0, s);
         else
             e0 = e1 = nullptr;

@@ -243,6 +243,7 @@ __device__ __forceinline__ void tmem_ld_wait(float (&v)[32])
 }
 
 struct TcArgs {
+    float* zout;            // MODE 3: [n_q][128] fp32, the first 128 accumulator columns of each row
     const float* qnorm;     // [n_q]
     const float* rnorm;     // [n_r]
     int64_t nq, nr;
@@ -349,7 +350,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     // short K (single-part operands, KB <= 2 slabs: C4's d = 50, the projected coarse pass): the
     // query block's A slabs are loaded once, with tile 0, into the A regions of stages 0..KB-1 and
     // stay there; later tiles stream only B (halves the L2 -> SMEM bytes per tile at KB = 1)
-    const bool res_a = MODE != 1 && KB <= 2 && KB <= TC_STAGES;
+    const bool res_a = MODE != 1 && MODE != 3 && KB <= 2 && KB <= TC_STAGES;
 
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES);
     const uint32_t tfull0 = smem_u32(bars + 2 * TC_STAGES), tempty0 = smem_u32(bars + 2 * TC_STAGES + 2);
@@ -389,7 +390,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             // ------------------------------------------------ TMA producer
             // MODE 1 (split operands, rows [hi | lo] of 2 KB columns): per K slab two stages,
             // the hi parts (A_hi, B_hi) then the lo parts (A_lo, B_lo)
-            constexpr int PARTS = MODE == 1 ? 2 : 1;
+            constexpr int PARTS = (MODE == 1 || MODE == 3) ? 2 : 1;
             // (profiling knob UMAP_TC_DEBUG bit 2: references evict_last too; bit 3: both evict_normal)
             uint64_t pol_a = l2_policy_evict_last();
             uint64_t pol_b = (a.debug & 4) ? l2_policy_evict_last() : l2_policy_evict_first();
@@ -448,7 +449,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                                   (kb | kk) != 0);
                     }
                     ++g;
-                    if constexpr (MODE == 1) {
+                    if constexpr (MODE == 1 || MODE == 3) {
                         // lo stage: hi_q . lo_r (A of the hi stage, B of the lo stage) and
                         // lo_q . hi_r (A of the lo stage, B of the hi stage) into the same accumulator
                         const int s2 = g % TC_STAGES;
@@ -595,6 +596,39 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             }
         }
         if (valid && !a.chunk_block) a.amb_count[q * NP + half] = n_amb;
+    } else if constexpr (MODE == 3) {
+        // ---------------------------------------------------- GEMM out (warps 2..9)
+        // Z = X_c P with split operands (hi.hi + hi.lo + lo.hi, the trust projection): one
+        // reference "tile" holds P^T (rows >= 128 zero), the half-0 warps write their row's first
+        // 128 accumulator columns as fp32
+        const int quad = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const int row = quad * 32 + lane;
+        const int64_t q = q0 + row;
+        for (int t = 0; t < ntiles; ++t) {
+            const int b = t & 1;
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
+            if (half == 0) {
+#pragma unroll 1
+                for (int c = 0; c < 128; c += 32) {
+                    float v[32];
+                    tmem_ld32(taddr + c, v);
+                    if (q < a.nq) {
+                        float4* o = reinterpret_cast<float4*>(a.zout + q * 128 + c);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) o[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 2) mbar_arrive_remote(mapa_shared(tempty0 + 8 * b, 0));
+                else mbar_arrive(tempty0 + 8 * b);
+            }
+        }
     } else if constexpr (MODE == 2) {
         // ---------------------------------------------------- coarse tile flags (warps 2..9)
         // Single-BF16 pass over the hi operands (norms folded: accumulator = -d2~/2, error
@@ -921,6 +955,28 @@ __global__ void chunk_max_kernel(const float* __restrict__ v, int64_t n, float* 
 // zeros up to d_pad - 6, the folded norms (role 1 / 2) of zn = |z~|^2 (fp32 of the fp32 z~); and
 // the per-row slack bvec = sigma (1.01 u |x_c|) + sqrt(K) gamma_d sigma |x_c| covering the
 // centring rounding and the fp32 projection error (|x_c|^2 = xnorm, the split operands' norms).
+// P^T (the d x 128 basis, fp32 row-major) as the split B operand of the tensor-core projection:
+// row c < 128 = [hi | lo] of column c (bf16(v), bf16(v - hi)), the d_pad - d padding columns and the
+// rows >= 128 zero (the caller clears the buffer), so the folded norms of the X operand add nothing
+__global__ void pt_split_kernel(const float* __restrict__ P, int d, int d_pad, __nv_bfloat16* __restrict__ Pt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d * 128) return;
+    const int f = i >> 7, c = i & 127;
+    const float v = P[i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    Pt[(int64_t)c * 2 * d_pad + f] = hi;
+    Pt[(int64_t)c * 2 * d_pad + d_pad + f] = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+// row of Z (in the reference operand's row order) holding query i: pos_of[qrow[i]], or row_begin + i
+__global__ void zrow_map_kernel(const int32_t* __restrict__ qrow, const int32_t* __restrict__ pos_of, int64_t rows,
+                                int64_t row_begin, int32_t* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows) out[i] = qrow ? pos_of[qrow[i]] : (int32_t)(row_begin + i);
+}
+
 __global__ void proj_operand_kernel(const float* __restrict__ Z, int KP, int K, int64_t rows, int d_pad,
                                     const int32_t* __restrict__ rowmap, const float* __restrict__ xnorm,
                                     const float* __restrict__ sigma_p, float gamma_d, int role, __nv_bfloat16* __restrict__ Zb, float* __restrict__ zn,
@@ -1272,7 +1328,8 @@ umap_status launch_tc_t(const CUtensorMap& mq, const CUtensorMap& mr, const TcAr
         UMAP_CUDA_TRY(cudaFuncSetAttribute(knn_tc_kernel<KC, ST, MODE, CG>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    ProfScope ps(MODE == 0 ? PROF_KNN_TC : (MODE == 1 ? PROF_TRUST_TC : PROF_TRUST_COARSE), s);
+    // MODE 3 runs inside the caller's projection scope (PROF_TRUST_PROJ)
+    ProfScope ps(MODE == 0 ? PROF_KNN_TC : (MODE == 1 ? PROF_TRUST_TC : (MODE == 2 ? PROF_TRUST_COARSE : -1)), s);
     if constexpr (CG == 2) {
         grid.x = (grid.x + 1) & ~1u;  // whole pairs; a pair's second block may lie past n_q (masked)
         cudaLaunchConfig_t cfg{};
@@ -1822,7 +1879,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             KPJ = atoi(e) <= 58 ? 58 : 122;
             DPZ = KPJ + 6;
         }
-        Scratch pbp, zf, zq, zr, znq, znr, pbq, pbr, cmr, cmb, psig;
+        Scratch pbp, zf, zq, zr, znq, znr, pbq, pbr, cmr, cmb, psig, pts, zrm;
         CUtensorMap map_zq, map_zr;
         bool projected = false;
         if (d >= 256 && !getenv("UMAP_TC_NO_PROJ")) {
@@ -1831,25 +1888,42 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             UMAP_TRY(psig.alloc(sizeof(float), s));
             const float* sigma = psig.as<float>();
             if (pca_basis(X, n, d, colsum.as<double>(), KPJ, pbp.as<float>(), psig.as<float>(), s) == UMAP_OK) {
+                // Z = X_c P on the tensor cores: the split reference operand (rows [hi | lo] of x_c, in
+                // its own row order) times the split P^T (one 256-row "tile", rows >= 128 zero), three
+                // products per K slab (MODE 3); per component |z~ - z| <= gamma_tc sigma |x_c| with
+                // gamma_tc = (3 2^-16 representation + 3 d_pad products x 2u accumulated onto sums up to
+                // 1.016 |x_c| sigma) x 1.05
                 UMAP_TRY(zf.alloc(sizeof(float) * (size_t)n * KPG, s));
-                tgemm128_kernel<false><<<(unsigned)ceil_div(n, 128), 256, 0, s>>>(X, n, 1, d, d, colsum.as<double>(),
-                                                                                 1.0 / (double)n, pbp.as<float>(),
-                                                                                 zf.as<float>());
-                UMAP_LAUNCH_CHECK("tgemm128_kernel");
+                UMAP_TRY(pts.alloc(sizeof(__nv_bfloat16) * (size_t)256 * dk, s));
+                UMAP_CUDA_TRY(cudaMemsetAsync(pts.p, 0, sizeof(__nv_bfloat16) * (size_t)256 * dk, s));
+                pt_split_kernel<<<ceil_div(d * 128, 256), 256, 0, s>>>(pbp.as<float>(), d, d_pad, pts.as<__nv_bfloat16>());
+                UMAP_LAUNCH_CHECK("pt_split_kernel");
+                CUtensorMap map_xa, map_pt;
+                UMAP_TRY(make_map(&map_xa, xr.as<__nv_bfloat16>(), n, dk, TC_BM));
+                UMAP_TRY(make_map(&map_pt, pts.as<__nv_bfloat16>(), 256, dk, TC_BN / tc_cg()));
+                TcArgs az{};
+                az.zout = zf.as<float>();
+                az.nq = n; az.nr = 256; az.kblocks = d_pad / TC_BK; az.split_len = 256;
+                UMAP_TRY((launch_tc<32, 3>(map_xa, map_pt, az, dim3((unsigned)((n + TC_BM - 1) / TC_BM), 1), s)));
                 const double u = std::ldexp(1.0, -24);
-                const float gamma_d = (float)(d * u / (1.0 - d * u));
+                const float gamma_d = (float)((3.0 * std::ldexp(1.0, -16) + 6.0 * d_pad * u * 1.016) * 1.05);
+                UMAP_TRY(zrm.alloc(sizeof(int32_t) * (size_t)rows, s));
+                zrow_map_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(ordered ? qrow.as<int32_t>() : nullptr,
+                                                                   ordered ? pos_of.as<int32_t>() : nullptr, rows,
+                                                                   row_begin, zrm.as<int32_t>());
+                UMAP_LAUNCH_CHECK("zrow_map_kernel");
                 UMAP_TRY(zq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * DPZ, s));
                 UMAP_TRY(znq.alloc(sizeof(float) * (size_t)rows, s));
                 UMAP_TRY(pbq.alloc(sizeof(float) * (size_t)rows, s));
                 proj_operand_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(
-                    zf.as<float>(), KPG, KPJ, rows, DPZ, qrow.as<int32_t>(), qn.as<float>(), sigma, gamma_d, 1,
+                    zf.as<float>(), KPG, KPJ, rows, DPZ, zrm.as<int32_t>(), qn.as<float>(), sigma, gamma_d, 1,
                     zq.as<__nv_bfloat16>(), znq.as<float>(), pbq.as<float>());
                 UMAP_LAUNCH_CHECK("proj_operand_kernel");
                 UMAP_TRY(zr.alloc(sizeof(__nv_bfloat16) * (size_t)n * DPZ, s));
                 UMAP_TRY(znr.alloc(sizeof(float) * (size_t)n, s));
                 UMAP_TRY(pbr.alloc(sizeof(float) * (size_t)n, s));
                 proj_operand_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(
-                    zf.as<float>(), KPG, KPJ, n, DPZ, perm.as<int32_t>(), rn.as<float>(), sigma, gamma_d, 2,
+                    zf.as<float>(), KPG, KPJ, n, DPZ, nullptr, rn.as<float>(), sigma, gamma_d, 2,
                     zr.as<__nv_bfloat16>(), znr.as<float>(), pbr.as<float>());
                 UMAP_LAUNCH_CHECK("proj_operand_kernel");
                 UMAP_TRY(make_map(&map_zq, zq.as<__nv_bfloat16>(), rows, DPZ, TC_BM));
