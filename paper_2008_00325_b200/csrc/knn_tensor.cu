@@ -1009,16 +1009,20 @@ __global__ void proj_operand_kernel(const float* __restrict__ Z, int KP, int K, 
 // lo = bf16(x_c - hi), row layout [hi | lo] (2 d_pad columns).  The RANK kernel issues
 // hi.hi + hi.lo + lo.hi into one accumulator from the hi and lo K slabs (x.y to ~2^-16
 // relative); norms are the fp32 sums of x_c^2.
+// wnorm (optional): sum_f x_c,f^2 max(0, KB - 1 - f / 64) (KB = d_pad / 64 K slabs) = sum over
+// the first KB - 1 slabs k of the cumulative squared norm through slab k: the weighted norm of the
+// fine pass's per-pair accumulation bound
 __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int d_pad,
                                   const double* __restrict__ colsum, double inv_n,
                                   __nv_bfloat16* __restrict__ Xs, float* __restrict__ norms,
-                                  const int32_t* __restrict__ rowmap, int role)
+                                  const int32_t* __restrict__ rowmap, int role, float* __restrict__ wnorm = nullptr)
 {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const int64_t src = rowmap ? (int64_t)rowmap[row] : row;  // output row `row` holds input row `src`
-    float acc = 0.0f;
+    float acc = 0.0f, accw = 0.0f;
+    const int kbm1 = d_pad / TC_BK - 1;
     __nv_bfloat16* o = Xs + row * (int64_t)(2 * d_pad);
     for (int f = lane; f < d_pad; f += 32) {
         __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
@@ -1027,14 +1031,27 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
             hi = __float2bfloat16_rn(c);
             lo = __float2bfloat16_rn(c - __bfloat162float(hi));
             acc = fmaf(c, c, acc);
+            accw = fmaf(c * c, (float)max(0, kbm1 - f / TC_BK), accw);
         }
         o[f] = hi;
         o[d_pad + f] = lo;
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
+    if (wnorm) {
+        accw = warp_sum(accw);
+        if (lane == 0) wnorm[row] = accw;
+    }
     __syncwarp();
     write_norm_extras(o, d_pad, acc, role, lane);  // folded norms in the hi part; lo stays 0 there
+}
+
+// per-row error budget of the fine pass: e = cS |x_c|^2 + cW wnorm (E(q, r) = e_q + e_r)
+__global__ void err_budget_kernel(const float* __restrict__ nrm, const float* __restrict__ wn, int64_t n, float cS,
+                                  float cW, float* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (cS * nrm[i] + cW * wn[i]) * 1.0001f;
 }
 
 // ----------------------------------------------------------------------------- re-rank
@@ -1743,7 +1760,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     if (k > TC_KT) { *overflow = 1; return UMAP_OK; }
     const int d_pad = (d + 6 + TC_BK - 1) / TC_BK * TC_BK;  // >= 6 padding columns for the folded norms
     const int dk = 2 * d_pad;
-    Scratch colsum, xr, rn, xq, qn, amb, ambc;
+    Scratch colsum, xr, rn, xq, qn, amb, ambc, rw, qw, er, eq;
     Scratch perm, pos_of, keys, qperm, qrow, selfc, thr_p, thri_p, hist_p;
     const bool ordered = Y != nullptr && d_emb == 2 && n < (int64_t)INT32_MAX;
     if (ordered) {
@@ -1781,16 +1798,18 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     }
     UMAP_TRY(xr.alloc(sizeof(__nv_bfloat16) * (size_t)n * dk, s));
     UMAP_TRY(rn.alloc(sizeof(float) * (size_t)n, s));
+    UMAP_TRY(rw.alloc(sizeof(float) * (size_t)n, s));
+    UMAP_TRY(qw.alloc(sizeof(float) * (size_t)rows, s));
     split_bf16_kernel<<<ceil_div(n * 32, 256), 256, 0, s>>>(X, n, d, d_pad, colsum.as<double>(), 1.0 / (double)n,
                                                           xr.as<__nv_bfloat16>(), rn.as<float>(),
-                                                          ordered ? perm.as<int32_t>() : nullptr, 2);
+                                                          ordered ? perm.as<int32_t>() : nullptr, 2, rw.as<float>());
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
     split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(ordered ? X : X + row_begin * (int64_t)d, rows, d,
                                                              d_pad, colsum.as<double>(), 1.0 / (double)n,
                                                              xq.as<__nv_bfloat16>(), qn.as<float>(),
-                                                             ordered ? qrow.as<int32_t>() : nullptr, 1);
+                                                             ordered ? qrow.as<int32_t>() : nullptr, 1, qw.as<float>());
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
@@ -1810,6 +1829,9 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     a.self_col = ordered ? selfc.as<int32_t>() : nullptr;
     // certification margin c: |d2~ - R2(q, r)| <= c (|q|^2 + |r|^2) under any
     // accumulation order with round-to-nearest or truncating fp32 adds (u = 2^-24):
+    // tuning/A-B knob UMAP_TC_FLAT_MARGIN=1: the uniform margin c (|q|^2 + |r|^2) of round 1
+    bool per_pair = !getenv("UMAP_TC_FLAT_MARGIN");
+    float cS_f = 0.0f, cW_f = 0.0f;
     // split representation + accumulation of 3 d_pad products + norms + R2's own error + final ops,
     // times 1.1 (C2: 2.94e-4)
     {
@@ -1820,6 +1842,17 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         const double c = 3.0 * std::ldexp(1.0, -16) * 0.5 + 3.0 * d_pad * 2.0 * u * 0.5 +
                          ((d + 31) / 32 + 5) * u + 2.0 * u + 0.5 * u + 144.0 * 2.0 * u + 4.0 * u;
         a.margin = (float)(1.1 * c);
+        // per-pair form (round 2, the default): the MMAs accumulate slab by slab, so the adds of
+        // slab k < KB land on partial sums bounded by the products of slabs 1..k,
+        // 1.016 (Q_k + R_k) / 2 (Q_k = |q|^2 through slab k): 192 adds x 2u each; only the last
+        // slab (with the folded norms) adds onto partial sums up to 1.008 S.  So
+        // E(q, r) = 1.1 (cS S + cW (Qw_q + Qw_r)), Qw = sum_{k < KB} Q_k (split_bf16's wnorm),
+        // cS = split representation + last slab 192 x 2u x 1.008 + norms + final ops + centring,
+        // cW = 192 x 2u x 1.016 / 2 -- instead of 2496 adds onto partial sums up to S / 2 each
+        // (C2: E ~ 1.35e-4 S instead of 2.10e-4 S for rows with their mass spread over the features)
+        cS_f = (float)(1.1 * (3.0 * std::ldexp(1.0, -16) * 0.5 + 192.0 * 2.0 * u * 1.008 + ((d + 31) / 32 + 5) * u +
+                              2.0 * u + 0.5 * u + 4.0 * u));
+        cW_f = (float)(1.1 * 192.0 * 2.0 * u * 1.016 * 0.5);
         // R2's own error, relative to d2 itself rather than 2S: |R2 - d2| <= gamma_{d+1} d2, times
         // 1.1, plus 4u for the fp32 difference and product that apply the factors and the
         // factors' own rounding
@@ -1831,8 +1864,24 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             a.r_lo = a.r_hi = 1.0f;
         }
     }
+    if (const char* mg = unsafe_env("UMAP_TRUST_MARGIN_EXPERIMENT")) {  // measurement only (uniform form)
+        a.margin = (float)atof(mg);
+        per_pair = false;
+    }
+    if (per_pair) {
+        // E(q, r) = e_q + e_r through the kernel's c_m (qnorm + rnorm) with c_m = 1
+        UMAP_TRY(er.alloc(sizeof(float) * (size_t)n, s));
+        UMAP_TRY(eq.alloc(sizeof(float) * (size_t)rows, s));
+        err_budget_kernel<<<ceil_div(n, 256), 256, 0, s>>>(rn.as<float>(), rw.as<float>(), n, cS_f, cW_f, er.as<float>());
+        UMAP_LAUNCH_CHECK("err_budget_kernel");
+        err_budget_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qn.as<float>(), qw.as<float>(), rows, cS_f, cW_f,
+                                                             eq.as<float>());
+        UMAP_LAUNCH_CHECK("err_budget_kernel");
+        a.qnorm = eq.as<float>();
+        a.rnorm = er.as<float>();
+        a.margin = 1.0f;
+    }
     a.thr_d2 = thr_use; a.k = k;
-    if (const char* mg = unsafe_env("UMAP_TRUST_MARGIN_EXPERIMENT")) a.margin = (float)atof(mg);  // measurement only
     a.hist = hist_use; a.amb = amb.as<int32_t>(); a.amb_cap = cap;
     if (const char* dbg = unsafe_env("UMAP_TC_DEBUG")) a.debug = atoi(dbg);  // profiling only (results invalid)
     a.dense_min = TC_DENSE_MIN;
@@ -1851,6 +1900,8 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         UMAP_TRY(tl.alloc(sizeof(int32_t) * (size_t)nqb * ntl, s));
         UMAP_TRY(tcnt.alloc(sizeof(int32_t) * (size_t)nqb, s));
         TcArgs ac = a;
+        ac.qnorm = qn.as<float>();  // the coarse pass's own margin applies to the squared norms
+        ac.rnorm = rn.as<float>();
         ac.kblocks = d_pad / TC_BK;   // hi part only
         ac.flags = flags.as<uint8_t>();
         ac.tile_ld = (int)ntl;
@@ -1993,8 +2044,14 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                 UMAP_LAUNCH_CHECK("shard_order_kernel");
                 split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(X, rows, d, d_pad, colsum.as<double>(),
                                                                          1.0 / (double)n, xq.as<__nv_bfloat16>(),
-                                                                         qn.as<float>(), qrow.as<int32_t>(), 1);
+                                                                         qn.as<float>(), qrow.as<int32_t>(), 1,
+                                                                         qw.as<float>());
                 UMAP_LAUNCH_CHECK("split_bf16_kernel");
+                if (per_pair) {
+                    err_budget_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qn.as<float>(), qw.as<float>(), rows, cS_f,
+                                                                         cW_f, eq.as<float>());
+                    UMAP_LAUNCH_CHECK("err_budget_kernel");
+                }
                 block_flags_kernel<<<(unsigned)nqb, 256, 0, s>>>(rowfl.as<uint8_t>(), pos2.as<int32_t>(), rows,
                                                                  (int)ntl, flags.as<uint8_t>());
                 UMAP_LAUNCH_CHECK("block_flags_kernel");
