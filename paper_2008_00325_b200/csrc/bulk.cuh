@@ -112,6 +112,54 @@ __device__ __forceinline__ float exact_d2_bulk(const float* __restrict__ x, cons
 }
 
 
+// Two query rows per warp (k <= 15 candidates each): lanes 0..14 pair x0 with Xr[l_lane], lanes
+// 16..30 pair x1 with Xr[l_lane]; x0 goes to the ring's query slot (32), x1 to lane 31's slot (lanes
+// 15 and 31 carry no candidate).  Otherwise exact_d2_bulk.
+__device__ __forceinline__ float exact_d2_bulk2(const float* __restrict__ x0, const float* __restrict__ x1,
+                                                const float* __restrict__ Xr, int32_t l, int d, float* ring,
+                                                uint32_t bar0, uint32_t& ph, int lane)
+{
+    const unsigned act = __ballot_sync(0xffffffffu, l >= 0);
+    const int nch = (d + RB_CH - 1) / RB_CH;
+    const int qslot = lane < 16 ? 32 : 31;
+    auto issue = [&](int c) {
+        const int b = c & 1;
+        const int w = min(RB_CH, d - c * RB_CH);
+        const uint32_t bytes = (uint32_t)w * 4u;
+        const uint32_t bar = bar0 + 8 * b;
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(ring + (size_t)b * 33 * RB_CH);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads vs the async refill
+        __syncwarp();
+        if (lane == 0) {
+            mbar_expect_tx(bar, bytes * (uint32_t)(__popc(act) + 2));
+            bulk_g2s(base + 32u * RB_CH * 4u, x0 + (size_t)c * RB_CH, bytes, bar);
+            bulk_g2s(base + 31u * RB_CH * 4u, x1 + (size_t)c * RB_CH, bytes, bar);
+        }
+        __syncwarp();
+        if (l >= 0) bulk_g2s(base + (uint32_t)lane * RB_CH * 4u, Xr + (int64_t)l * d + (size_t)c * RB_CH, bytes, bar);
+    };
+    issue(0);
+    float s = 0.0f;
+    for (int c = 0; c < nch; ++c) {
+        const int b = c & 1;
+        if (c + 1 < nch) issue(c + 1);
+        mbar_wait(bar0 + 8 * b, (ph >> b) & 1u);
+        ph ^= 1u << b;
+        const float4* rr = reinterpret_cast<const float4*>(ring + (size_t)b * 33 * RB_CH + (size_t)lane * RB_CH);
+        const float4* xx = reinterpret_cast<const float4*>(ring + (size_t)b * 33 * RB_CH + (size_t)qslot * RB_CH);
+        const int w4 = min(RB_CH, d - c * RB_CH) >> 2;
+        for (int j = 0; j < w4; ++j) {
+            const float4 a = xx[j], y = rr[j];
+            float t = __fsub_rn(a.x, y.x); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.y, y.y); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.z, y.z); s = __fmaf_rn(t, t, s);
+            t = __fsub_rn(a.w, y.w); s = __fmaf_rn(t, t, s);
+        }
+        __syncwarp();  // every lane is done with buffer b before it is refilled
+    }
+    return s;
+}
+
 // per-warp ring of a block of RB_WARPS warps (dynamic smem of RB_SMEM bytes); initialises the
 // warp's two mbarriers (lane 0) and returns the ring and the first barrier's address
 __device__ __forceinline__ float* bulk_ring_setup(uint32_t& bar0)

@@ -197,6 +197,24 @@ __device__ __forceinline__ void warp_bitonic(float& key, int32_t& id, int lane)
 }
 
 
+// two independent ascending bitonic sorts of (key, id) over lanes 0..15 and 16..31
+__device__ __forceinline__ void warp_bitonic16(float& key, int32_t& id, int lane)
+{
+#pragma unroll
+    for (int size = 2; size <= 16; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const float ok = __shfl_xor_sync(0xffffffffu, key, stride);
+            const int32_t oi = __shfl_xor_sync(0xffffffffu, id, stride);
+            const bool up = size == 16 || ((lane & size) == 0);
+            const bool lower = (lane & stride) == 0;
+            const bool other_less = key_less(ok, oi, key, id);
+            const bool take = lower ? (up ? other_less : !other_less) : (up ? !other_less : other_less);
+            if (take && !(ok == key && oi == id)) { key = ok; id = oi; }
+        }
+    }
+}
+
 inline unsigned ceil_div(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 // Measurement knobs that make results invalid or uncertified (margin overrides, disabled

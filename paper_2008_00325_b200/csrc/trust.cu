@@ -58,6 +58,28 @@ __global__ void thresholds_warp_kernel(const float* __restrict__ X, int d, const
     const int lane = threadIdx.x & 31;
     uint32_t bar0 = 0, ph = 0;
     float* ring = bulk ? bulk_ring_setup(bar0) : nullptr;
+    if (bulk == 2) {
+        // k <= 15: two rows per warp (lanes 0..14 and 16..30), both query rows through the ring
+        const int64_t w0 = 2 * w, w1 = 2 * w + 1;
+        if (w0 >= rows) return;
+        const int h = lane >> 4, li = lane & 15;
+        const int64_t wh = h ? w1 : w0;
+        const bool okrow = wh < rows;
+        const int64_t r0 = order ? (int64_t)order[w0] : w0;
+        const int64_t r1 = w1 < rows ? (order ? (int64_t)order[w1] : w1) : r0;
+        const int64_t r = h ? r1 : r0;
+        const int32_t j = (okrow && li < k) ? emb_idx[r * k + li] : -1;
+        const float v = exact_d2_bulk2(X + (row_begin + r0) * (int64_t)d, X + (row_begin + r1) * (int64_t)d, X, j, d,
+                                       ring, bar0, ph, lane);
+        float key = j >= 0 ? v : INFINITY;
+        int32_t id = j >= 0 ? j : INT32_MAX;
+        warp_bitonic16(key, id, lane);
+        if (okrow && li < k) {
+            thr_d2[r * k + li] = key;
+            thr_id[r * k + li] = id;
+        }
+        return;
+    }
     if (w >= rows) return;
     // order (optional): rows visited in the Hilbert order of the embedding, so the warps
     // resident at one time gather neighbour rows of the same 2-D region (L2 reuse)
@@ -123,7 +145,10 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
         ProfScope ps(PROF_THRESHOLDS, s);
         // the bulk ring measured slower here (0.79 vs 0.72 ms at C2: k = 15 of 32 lanes busy,
         // one batch per row), so the per-lane streaming path is used; the option stays for k > 16
-        const bool bulk = k > 16 && (d % 4 == 0) && ((uintptr_t)X % 16 == 0);
+        // k <= 15: two rows per warp through the bulk ring (tuning knob UMAP_TRUST_THR2=0: streaming)
+        const bool aligned = (d % 4 == 0) && ((uintptr_t)X % 16 == 0);
+        const bool two = k <= 15 && aligned && !(getenv("UMAP_TRUST_THR2") && atoi(getenv("UMAP_TRUST_THR2")) == 0);
+        const bool bulk = (k > 16 && aligned) || two;
         if (bulk) {
             static PerDeviceOnce cfg;
             if (cfg.first()) {
@@ -131,8 +156,9 @@ umap_status trust_penalty(const float* X, int64_t n, int d, const int32_t* emb_i
                                                    (int)RB_SMEM));
             }
         }
-        thresholds_warp_kernel<<<ceil_div(rows * 32, 32 * RB_WARPS), 32 * RB_WARPS, bulk ? RB_SMEM : 0, s>>>(
-            X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(), thr_i.as<int32_t>(), bulk ? 1 : 0,
+        const int64_t warps = two ? (rows + 1) / 2 : rows;
+        thresholds_warp_kernel<<<ceil_div(warps * 32, 32 * RB_WARPS), 32 * RB_WARPS, bulk ? RB_SMEM : 0, s>>>(
+            X, d, emb_idx, rows, row_begin, k, thr_d.as<float>(), thr_i.as<int32_t>(), two ? 2 : (bulk ? 1 : 0),
             ordered && k <= 32 ? order.as<int32_t>() : nullptr);
         UMAP_LAUNCH_CHECK("thresholds_warp_kernel");
     } else {
