@@ -1054,6 +1054,27 @@ __global__ void err_budget_kernel(const float* __restrict__ nrm, const float* __
     if (i < n) out[i] = (cS * nrm[i] + cW * wn[i]) * 1.0001f;
 }
 
+// out[0] += sum of the per-(row, part) ambiguous counts, out[1] |= any count > cap
+__global__ void amb_reduce_kernel(const int* __restrict__ cnt, int64_t m, int cap, unsigned long long* __restrict__ out)
+{
+    unsigned long long sum = 0;
+    int over = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = cnt[i];
+        sum += (unsigned long long)c;
+        over |= c > cap;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        over |= __shfl_xor_sync(0xffffffffu, over, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (sum) atomicAdd(out, sum);
+        if (over) atomicOr(out + 1, 1ull);
+    }
+}
+
 // ----------------------------------------------------------------------------- re-rank
 // warp per query row; candidates t and t + 32 on lane t (kc <= 64); exact fp32 d2 (R2),
 // a bitonic sort of each 32-wide half by key (d2, id), then the two sorted halves are
@@ -2144,15 +2165,19 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                                                                   hist);
         UMAP_LAUNCH_CHECK("unscatter_hist_kernel");
     }
-    std::vector<int> counts((size_t)rows * NL);
-    UMAP_CUDA_TRY(cudaMemcpyAsync(counts.data(), ambc.p, sizeof(int) * rows * NL, cudaMemcpyDeviceToHost, s));
+    // the re-checked pair total and the list overflow flag, reduced on the device (16 bytes back
+    // instead of the rows x NL counts)
+    Scratch red;
+    UMAP_TRY(red.alloc(sizeof(unsigned long long) * 2, s));
+    UMAP_CUDA_TRY(cudaMemsetAsync(red.p, 0, sizeof(unsigned long long) * 2, s));
+    amb_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * NL, 256), 4 * num_sms()), 256, 0, s>>>(
+        ambc.as<int>(), rows * NL, cap, red.as<unsigned long long>());
+    UMAP_LAUNCH_CHECK("amb_reduce_kernel");
+    unsigned long long hr[2] = {0, 0};
+    UMAP_CUDA_TRY(cudaMemcpyAsync(hr, red.p, sizeof(hr), cudaMemcpyDeviceToHost, s));
     UMAP_CUDA_TRY(cudaStreamSynchronize(s));
-    int64_t total = 0;
-    for (int c : counts) {
-        total += c;
-        if (c > cap) *overflow = 1;
-    }
-    g_last_rank_ambiguous = total;
+    if (hr[1]) *overflow = 1;
+    g_last_rank_ambiguous = (int64_t)hr[0];
     return UMAP_OK;
 }
 
