@@ -1075,6 +1075,18 @@ __global__ void amb_reduce_kernel(const int* __restrict__ cnt, int64_t m, int ca
     }
 }
 
+// query i's squared norm and weighted norm from the reference pass: row pos_of[qrow[i]]
+__global__ void gather_norms_kernel(const int32_t* __restrict__ qrow, const int32_t* __restrict__ pos_of, int64_t rows,
+                                    const float* __restrict__ rn, const float* __restrict__ rw, float* __restrict__ qn,
+                                    float* __restrict__ qw)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int32_t p = pos_of[qrow[i]];
+    qn[i] = rn[p];
+    qw[i] = rw[p];
+}
+
 // ----------------------------------------------------------------------------- re-rank
 // warp per query row; candidates t and t + 32 on lane t (kc <= 64); exact fp32 d2 (R2),
 // a bitonic sort of each 32-wide half by key (d2, id), then the two sorted halves are
@@ -1827,11 +1839,28 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
     UMAP_LAUNCH_CHECK("split_bf16_kernel");
     UMAP_TRY(xq.alloc(sizeof(__nv_bfloat16) * (size_t)rows * dk, s));
     UMAP_TRY(qn.alloc(sizeof(float) * (size_t)rows, s));
-    split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(ordered ? X : X + row_begin * (int64_t)d, rows, d,
-                                                             d_pad, colsum.as<double>(), 1.0 / (double)n,
-                                                             xq.as<__nv_bfloat16>(), qn.as<float>(),
-                                                             ordered ? qrow.as<int32_t>() : nullptr, 1, qw.as<float>());
-    UMAP_LAUNCH_CHECK("split_bf16_kernel");
+    // the query operand (role 1): in an ordered run its rows are reference rows (pos_of[qrow[i]]), so
+    // the norms are gathered from the reference pass and the operand itself is built only when a
+    // pass reads it (the projected coarse pass does not; the regroup rebuilds it in its own order)
+    bool xq_built = false;
+    auto build_xq = [&]() -> umap_status {
+        split_bf16_kernel<<<ceil_div(rows * 32, 256), 256, 0, s>>>(ordered ? X : X + row_begin * (int64_t)d, rows, d,
+                                                                 d_pad, colsum.as<double>(), 1.0 / (double)n,
+                                                                 xq.as<__nv_bfloat16>(), qn.as<float>(),
+                                                                 ordered ? qrow.as<int32_t>() : nullptr, 1,
+                                                                 qw.as<float>());
+        UMAP_LAUNCH_CHECK("split_bf16_kernel");
+        xq_built = true;
+        return UMAP_OK;
+    };
+    if (ordered) {
+        gather_norms_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qrow.as<int32_t>(), pos_of.as<int32_t>(), rows,
+                                                               rn.as<float>(), rw.as<float>(), qn.as<float>(),
+                                                               qw.as<float>());
+        UMAP_LAUNCH_CHECK("gather_norms_kernel");
+    } else {
+        UMAP_TRY(build_xq());
+    }
     CUtensorMap map_q, map_r;
     UMAP_TRY(make_map(&map_q, xq.as<__nv_bfloat16>(), rows, dk, TC_BM));
     UMAP_TRY(make_map(&map_r, xr.as<__nv_bfloat16>(), n, dk, TC_BN / tc_cg()));
@@ -2025,6 +2054,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
         if (projected) {
             UMAP_TRY((launch_tc<32, 2>(map_zq, map_zr, ac, dim3((unsigned)qblocks, 1), s)));
         } else {
+            if (!xq_built) UMAP_TRY(build_xq());
             UMAP_TRY((launch_tc<32, 2>(map_q, map_r, ac, dim3((unsigned)qblocks, 1), s)));
         }
         if (regroup) {
@@ -2068,6 +2098,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
                                                                          qn.as<float>(), qrow.as<int32_t>(), 1,
                                                                          qw.as<float>());
                 UMAP_LAUNCH_CHECK("split_bf16_kernel");
+                xq_built = true;
                 if (per_pair) {
                     err_budget_kernel<<<ceil_div(rows, 256), 256, 0, s>>>(qn.as<float>(), qw.as<float>(), rows, cS_f,
                                                                          cW_f, eq.as<float>());
@@ -2127,6 +2158,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             UMAP_CUDA_TRY(cudaMemsetAsync(hist_use, 0, sizeof(int32_t) * (size_t)rows * k, s));
             UMAP_CUDA_TRY(cudaMemsetAsync(ambc.p, 0, sizeof(int) * (size_t)rows * NL, s));
         }
+        if (!xq_built) UMAP_TRY(build_xq());
         UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)(a.chunk_block ? 2 * nchunks : qblocks), 1), s)));
         double m = 0;
         for (int32_t x : cn) m += x;
@@ -2135,6 +2167,7 @@ umap_status rank_count_tc(const float* X, int64_t n, int d, int64_t row_begin, i
             fprintf(stderr, "[coarse] %.1f of %lld tiles kept per block\n", m / nqb, (long long)ntl);
     } else {
         g_last_fine_fraction = 1.0;
+        if (!xq_built) UMAP_TRY(build_xq());
         UMAP_TRY((launch_tc<32, 1>(map_q, map_r, a, dim3((unsigned)qblocks, 1), s)));
     }
     {
