@@ -468,6 +468,29 @@ def test_trust_tensor_exact_penalty(O, n, d, k, kind, emb):
     assert np.array_equal(np_(pen3), pen_ref[17:300]) and S3 == S2
 
 
+@pytest.mark.parametrize("profile", ["front", "back", "spike"])
+def test_trust_tensor_per_pair_margin_adversarial(O, profile):
+    """The per-pair fine-pass margin charges each slab's adds with the products of
+    the slabs before it: rows whose squared norm sits in the first features (front: the largest
+    Qw, partial sums near their maximum from the first slab on), in the last ones (back) or in one
+    feature (spike) must still give exactly the oracle's penalty, as must the uniform form."""
+    n, d, k = 1400, 784, 15
+    X = synth.lowrank(n, d, blobs=10, seed=31)
+    f = np.arange(d, dtype=np.float32)
+    if profile == "front":
+        w = np.exp(-f / 40.0)
+    elif profile == "back":
+        w = np.exp(-(d - 1 - f) / 40.0)
+    else:
+        w = np.full(d, 0.05, np.float32)
+        w[5] = 30.0
+    X = np.ascontiguousarray(X * w[None, :].astype(np.float32), dtype=np.float32)
+    Y = synth.uniform_embedding(n, 2, seed=8)
+    S_ref, _ = O.trust_penalty(X, Y, k)
+    T, S = U.trustworthiness(cu(X), cu(Y), k, knn_mode="tensor")
+    assert S == S_ref
+
+
 def test_trust_tensor_table4_shape_and_overflow_fallback(O, monkeypatch):
     """Table-4-shaped rows (isotropic blobs, d = 1024): the tensor path's penalty equals the
     oracle's; with the re-check lists shrunk to 2 pairs per list the tensor pass overflows and
