@@ -345,7 +345,12 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     // (in pivot order: its own neighbourhood) and wraps around; the same for both CTAs of a pair
     const int rot0 = (a.rotate && !tlist && ntiles_all > 0)
                          ? (int)(((int64_t)pblk * 2 * TC_BM * ntiles_all / (a.nq > 0 ? a.nq : 1)) % ntiles_all) : 0;
-    auto tile_at = [&](int t) { return tlist ? tlist[t] : (rot0 ? (t + rot0) % ntiles_all : t); };
+    // (t + rot0 < 2 ntiles_all: one conditional subtraction, no integer division per tile)
+    auto tile_at = [&](int t) {
+        if (tlist) return (int)tlist[t];
+        const int u = t + rot0;
+        return u >= ntiles_all ? u - ntiles_all : u;
+    };
     const int KB = a.kblocks;
     // short K (single-part operands, KB <= 2 slabs: C4's d = 50, the projected coarse pass): the
     // query block's A slabs are loaded once, with tile 0, into the A regions of stages 0..KB-1 and
