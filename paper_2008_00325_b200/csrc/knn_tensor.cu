@@ -740,6 +740,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
 #pragma unroll
         for (int i = 0; i < KC; ++i) { kd[i] = INFINITY; ki[i] = -1; }
         float thr = INFINITY;
+        const bool prefilter = a.prefilter != 0, dbg_skip = (a.debug & 1) != 0;  // hoisted out of the chunk loop
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
             mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
@@ -805,7 +806,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             // and are skipped after one vote); out-of-range columns (zero-filled TMA rows) are
             // masked by their index
 #pragma unroll 1
-            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !(a.debug & 1); c += 64) {
+            for (int c = half * (TC_BN / 2); c < (half + 1) * (TC_BN / 2) && !dbg_skip; c += 64) {
                 float v0[32], v1[32];
                 tmem_ld32_nw(taddr + c, v0);
                 tmem_ld32_nw(taddr + c + 32, v1);
@@ -813,7 +814,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 tmem_ld_wait(v1);
                 const int64_t jb = rb + c;
                 bool p0 = true, p1 = true;
-                if (a.prefilter) {
+                if (prefilter) {
                     const float nthr = -0.5f * thr;
                     const float m0 = cmax(v0), m1 = cmax(v1);
                     p0 = __any_sync(0xffffffffu, valid && m0 > nthr);
