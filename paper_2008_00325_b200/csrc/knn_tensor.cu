@@ -790,16 +790,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             };
             // 32-column chunk maximum (31-op tree): the accumulator holds -d2/2, so a chunk with
             // max <= -thr/2 holds no candidate for this row
+            // as a tree of 3-input maxima (FMNMX3): 11 + 4 + 2 + 1 = 18 instructions for 32 values
             auto cmax = [](const float (&v)[32]) {
-                float m16[16];
+                float m[11];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) m16[i] = fmaxf(v[2 * i], v[2 * i + 1]);
-#pragma unroll
-                for (int w = 8; w >= 1; w >>= 1) {
-#pragma unroll
-                    for (int i = 0; i < w; ++i) m16[i] = fmaxf(m16[i], m16[i + w]);
-                }
-                return m16[0];
+                for (int i = 0; i < 10; ++i) m[i] = fmaxf(fmaxf(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+                m[10] = fmaxf(v[30], v[31]);
+                const float a0 = fmaxf(fmaxf(m[0], m[1]), m[2]), a1 = fmaxf(fmaxf(m[3], m[4]), m[5]);
+                const float a2 = fmaxf(fmaxf(m[6], m[7]), m[8]), a3 = fmaxf(m[9], m[10]);
+                return fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
             };
             // two chunks per step: both TMEM loads in flight before one wait, two independent max
             // trees (the short-K prefilter: most chunks hold no candidate for any row of the warp
