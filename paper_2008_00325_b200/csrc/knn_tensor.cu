@@ -396,9 +396,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             // MODE 1 (split operands, rows [hi | lo] of 2 KB columns): per K slab two stages,
             // the hi parts (A_hi, B_hi) then the lo parts (A_lo, B_lo)
             constexpr int PARTS = (MODE == 1 || MODE == 3) ? 2 : 1;
-            // (profiling knob UMAP_TC_DEBUG bit 2: references evict_last too; bit 3: both evict_normal)
+            // both operands evict_last (round 2: the reference tiles as evict_first measured 1 % slower
+            // at C2; profiling knob UMAP_TC_DEBUG bit 4: references evict_first, bit 3: both evict_normal)
             uint64_t pol_a = l2_policy_evict_last();
-            uint64_t pol_b = (a.debug & 4) ? l2_policy_evict_last() : l2_policy_evict_first();
+            uint64_t pol_b = (a.debug & 16) ? l2_policy_evict_first() : l2_policy_evict_last();
             if (a.debug & 8) {
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_a));
                 pol_b = pol_a;
