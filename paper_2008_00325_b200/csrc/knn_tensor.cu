@@ -157,26 +157,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
             : "memory");
     }
 }
-// the MMA issuer's wait for a free accumulator: no suspend-time hint (lowest wake-up latency for
-// the one thread the epilogue's next tile depends on)
-__device__ __forceinline__ void mbar_wait_cluster_spin(uint32_t bar, uint32_t parity)
-{
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void mbar_wait_spin(uint32_t bar, uint32_t parity)
-{
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
 // TMA load whose completion bytes go to the leader CTA's mbarrier (cluster address)
 __device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar_cluster,
                                                 uint64_t pol)
@@ -351,15 +331,6 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
     const bool leader = rank == 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // pipeline waits: plain try_wait polls (lowest wake-up latency: C2 / C4 kNN -2 %), except in the
-    // split-precision pass (16 epilogue warps share the schedulers with the polling threads: the
-    // 10 ms suspend-time hint of bulk.cuh's mbar_wait measured slightly better); UMAP_TC_DEBUG
-    // bit 5: the hint everywhere
-    const bool hint_waits = MODE == 1 || (a.debug & 32) != 0;
-    auto mbar_wait_k = [&](uint32_t bar, uint32_t parity) {
-        if (hint_waits) mbar_wait(bar, parity);
-        else mbar_wait_spin(bar, parity);
-    };
     // chunked fine pass (chunk_block != nullptr): CTA pair c works on tile-list chunk c of the
     // 256-row query block chunk_block[c]; chunks of one block run concurrently and add their counts
     const int64_t q0 = a.chunk_block ? ((int64_t)a.chunk_block[blockIdx.x >> 1] * 2 + (blockIdx.x & 1)) * TC_BM
@@ -425,10 +396,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             // MODE 1 (split operands, rows [hi | lo] of 2 KB columns): per K slab two stages,
             // the hi parts (A_hi, B_hi) then the lo parts (A_lo, B_lo)
             constexpr int PARTS = (MODE == 1 || MODE == 3) ? 2 : 1;
-            // both operands evict_last (round 2: the reference tiles as evict_first measured 1 % slower
-            // at C2; profiling knob UMAP_TC_DEBUG bit 4: references evict_first, bit 3: both evict_normal)
+            // queries evict_last, references evict_first (profiling knob UMAP_TC_DEBUG bit 2: references
+            // evict_last too, bit 3: both evict_normal; same-box A/B: evict_last references and
+            // hint-free polling waits measured no faster for C4 and slower for C2)
             uint64_t pol_a = l2_policy_evict_last();
-            uint64_t pol_b = (a.debug & 16) ? l2_policy_evict_first() : l2_policy_evict_last();
+            uint64_t pol_b = (a.debug & 4) ? l2_policy_evict_last() : l2_policy_evict_first();
             if (a.debug & 8) {
                 asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_a));
                 pol_b = pol_a;
@@ -441,7 +413,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     for (int part = 0; part < PARTS; ++part, ++g) {
                         const int s = g % TC_STAGES;
                         const uint32_t ph = (g / TC_STAGES) & 1;
-                        mbar_wait_k(empty0 + 8 * s, ph ^ 1);
+                        mbar_wait(empty0 + 8 * s, ph ^ 1);
                         const uint32_t dst = smem_u32(stage_base + s * STAGE_C);
                         const int x = (part * KB + kb) * TC_BK;
                         const bool load_a = !res_a || t == 0;
@@ -467,17 +439,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
             int g = 0;
             for (int t = 0; t < ntiles; ++t) {
                 const int b = t & 1;
-                if constexpr (CG == 2) {
-                    if (hint_waits) mbar_wait_cluster(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
-                    else mbar_wait_cluster_spin(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
-                }
-                else mbar_wait_k(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
+                if constexpr (CG == 2) mbar_wait_cluster(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
+                else mbar_wait(tempty0 + 8 * b, ((t >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(b * TC_BN);
                 for (int kb = 0; kb < KB; ++kb) {
                     const int s = g % TC_STAGES;
                     const uint32_t ph = (g / TC_STAGES) & 1;
-                    mbar_wait_k(full0 + 8 * s, ph);
+                    mbar_wait(full0 + 8 * s, ph);
                     tc_fence_after();
                     const uint32_t b_addr = smem_u32(stage_base + s * STAGE_C) + A_BYTES;
                     const uint32_t a_addr = smem_u32(stage_base + (res_a ? kb : s) * STAGE_C);
@@ -492,7 +461,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         // lo_q . hi_r (A of the lo stage, B of the hi stage) into the same accumulator
                         const int s2 = g % TC_STAGES;
                         const uint32_t ph2 = (g / TC_STAGES) & 1;
-                        mbar_wait_k(full0 + 8 * s2, ph2);
+                        mbar_wait(full0 + 8 * s2, ph2);
                         tc_fence_after();
                         const uint32_t a2 = smem_u32(stage_base + s2 * STAGE_C);
                         const uint32_t b2 = a2 + A_BYTES;
@@ -543,7 +512,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         int n_amb = 0;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
-            mbar_wait_k(tfull0 + 8 * b, (t >> 1) & 1);
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
             const int64_t rb = r_lo + (int64_t)tile_at(t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
@@ -645,7 +614,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const int64_t q = q0 + row;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
-            mbar_wait_k(tfull0 + 8 * b, (t >> 1) & 1);
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
             if (half == 0) {
@@ -686,7 +655,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const float aq = (proj && valid) ? *a.proj_sigma * sqrtf(tmax / a.r_lo) * 1.000001f + a.proj_bq[q] : 0.0f;
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
-            mbar_wait_k(tfull0 + 8 * b, (t >> 1) & 1);
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
             const int tile = tile_at(t);
             const int64_t rb = r_lo + (int64_t)tile * TC_BN;
@@ -776,7 +745,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
         const bool prefilter = a.prefilter != 0, dbg_skip = (a.debug & 1) != 0;  // hoisted out of the chunk loop
         for (int t = 0; t < ntiles; ++t) {
             const int b = t & 1;
-            mbar_wait_k(tfull0 + 8 * b, (t >> 1) & 1);
+            mbar_wait(tfull0 + 8 * b, (t >> 1) & 1);
             tc_fence_after();
             const int64_t rb = r_lo + (int64_t)tile_at(t) * TC_BN;
             const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * TC_BN);
