@@ -491,6 +491,27 @@ def test_trust_tensor_per_pair_margin_adversarial(O, profile):
     assert S == S_ref
 
 
+@pytest.mark.parametrize("tmaj,ch", [("0", "32"), ("0", "2"), ("1", "1"), ("1", "3")])
+def test_trust_tensor_fine_pass_chunk_orders(O, monkeypatch, tmaj, ch):
+    """The fine pass's work order: tile lists per query block in block order,
+    or chunks of CH tiles of every block launched tile-major (chunks of one block add into the
+    same rows concurrently); one-tile and ragged chunks included: the integer penalty must be the
+    oracle's whatever the order."""
+    n, d, k = 2100, 784, 15
+    X = synth.lowrank(n, d, blobs=12, seed=41)
+    Y = (X[:, :2] + np.random.default_rng(2).standard_normal((n, 2)) * 0.5).astype(np.float32)
+    S_ref, pen_ref = O.trust_penalty(X, Y, k)
+    monkeypatch.setenv("UMAP_TC_TILE_MAJOR", tmaj)
+    monkeypatch.setenv("UMAP_TC_CHUNK", ch)
+    T, S = U.trustworthiness(cu(X), cu(Y), k, knn_mode="tensor")
+    emb_idx, _ = O.knn(Y, Y, k, self_offset=0)
+    S2, pen = U.trust_penalty(cu(X), cu(emb_idx[40:1900]), k, 40, 1900, knn_mode="tensor", Y=cu(Y))
+    monkeypatch.delenv("UMAP_TC_TILE_MAJOR")
+    monkeypatch.delenv("UMAP_TC_CHUNK")
+    assert S == S_ref
+    assert np.array_equal(np_(pen), pen_ref[40:1900])
+
+
 def test_trust_tensor_table4_shape_and_overflow_fallback(O, monkeypatch):
     """Table-4-shaped rows (isotropic blobs, d = 1024): the tensor path's penalty equals the
     oracle's; with the re-check lists shrunk to 2 pairs per list the tensor pass overflows and
