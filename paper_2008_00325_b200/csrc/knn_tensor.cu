@@ -930,6 +930,7 @@ __global__ void center_bf16_kernel(const float* __restrict__ X, int64_t n, int d
     if (orow >= n) return;
     const int64_t row = rowmap ? (int64_t)rowmap[orow] : orow;  // input row
     float acc = 0.0f;
+#pragma unroll 4
     for (int f = lane; f < d_pad; f += 32) {
         __nv_bfloat16 h = __float2bfloat16_rn(0.0f);
         if (f < d) {
@@ -1031,17 +1032,44 @@ __global__ void split_bf16_kernel(const float* __restrict__ X, int64_t n, int d,
     float acc = 0.0f, accw = 0.0f;
     const int kbm1 = d_pad / TC_BK - 1;
     __nv_bfloat16* o = Xs + row * (int64_t)(2 * d_pad);
-    for (int f = lane; f < d_pad; f += 32) {
-        __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
-        if (f < d) {
-            const float c = X[src * d + f] - (float)(colsum[f] * inv_n);
-            hi = __float2bfloat16_rn(c);
-            lo = __float2bfloat16_rn(c - __bfloat162float(hi));
-            acc = fmaf(c, c, acc);
-            accw = fmaf(c * c, (float)max(0, kbm1 - f / TC_BK), accw);
+    if ((d & 1) == 0 && ((uintptr_t)X & 7) == 0) {
+        // feature pairs (2 lane, 2 lane + 1) + 64 i: 8-byte row loads, 4-byte bf16x2 stores; per lane
+        // d_pad / 32 terms in each sum, as in the scalar loop (the norm bound of DESIGN.md 7.1)
+        const float2* xr = reinterpret_cast<const float2*>(X + src * d);
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(o);
+        __nv_bfloat162* ol = reinterpret_cast<__nv_bfloat162*>(o + d_pad);
+#pragma unroll 4
+        for (int f = 2 * lane; f < d_pad; f += 64) {
+            float2 c = make_float2(0.0f, 0.0f);
+            if (f < d) {
+                const float2 x = xr[f >> 1];
+                c.x = x.x - (float)(colsum[f] * inv_n);
+                c.y = x.y - (float)(colsum[f + 1] * inv_n);
+                const float wgt = (float)max(0, kbm1 - f / TC_BK);  // f, f + 1 in one K slab
+                acc = fmaf(c.x, c.x, acc);
+                acc = fmaf(c.y, c.y, acc);
+                accw = fmaf(c.x * c.x, wgt, accw);
+                accw = fmaf(c.y * c.y, wgt, accw);
+            }
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(c.x, c.y);
+            const float2 hf = __bfloat1622float2(hi);
+            oh[f >> 1] = hi;
+            ol[f >> 1] = __floats2bfloat162_rn(c.x - hf.x, c.y - hf.y);
         }
-        o[f] = hi;
-        o[d_pad + f] = lo;
+    } else {
+#pragma unroll 4
+        for (int f = lane; f < d_pad; f += 32) {
+            __nv_bfloat16 hi = __float2bfloat16_rn(0.0f), lo = hi;
+            if (f < d) {
+                const float c = X[src * d + f] - (float)(colsum[f] * inv_n);
+                hi = __float2bfloat16_rn(c);
+                lo = __float2bfloat16_rn(c - __bfloat162float(hi));
+                acc = fmaf(c, c, acc);
+                accw = fmaf(c * c, (float)max(0, kbm1 - f / TC_BK), accw);
+            }
+            o[f] = hi;
+            o[d_pad + f] = lo;
+        }
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[row] = acc;
