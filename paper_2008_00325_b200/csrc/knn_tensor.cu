@@ -538,6 +538,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                 if (valid_cols < 32) cm &= valid_cols > 0 ? (0xffffffffu >> (32 - valid_cols)) : 0u;
                 if (!valid) cm = 0;
                 if (self_j >= jb && self_j < jb + 32) cm &= ~(1u << (uint32_t)(self_j - jb));
+                uint32_t am = 0;  // ambiguous columns of this chunk (re-checked exactly later)
                 if (__reduce_max_sync(0xffffffffu, (unsigned)__popc(cm)) >= (unsigned)a.dense_min) {
                     // dense chunk (the row's own cluster): every column bucketed, updates predicated
 #pragma unroll
@@ -547,11 +548,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                         const int b_lo = cnt_le16((v[u] - E) * a.r_lo, thr), b_hi = cnt_le16((v[u] + E) * a.r_hi, thr);
                         const bool act = (cm >> u) & 1u;
                         if (act && b_hi == b_lo && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
-                        if (act && b_hi != b_lo) {
-                            const int pos = a.chunk_block ? atomicAdd(a.amb_count + q * NP + half, 1) : n_amb;
-                            if (pos < a.amb_cap) amb_row[pos] = (int32_t)(jb + u);
-                            ++n_amb;
-                        }
+                        am |= (uint32_t)(act && b_hi != b_lo) << u;
                     }
                     cm = 0;
                 }
@@ -575,11 +572,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__
                     const int b_hi = cnt_le16(hiv, thr), b_lo = cnt_le16(lov, thr);  // #thresholds <= d2~ +- E
                     const bool amb = has && b_hi != b_lo;
                     if (has && !amb && b_lo < k) Hs[(half * TC_KT + b_lo) * TC_BM + row] += 1;
-                    if (amb) {
-                        const int pos = a.chunk_block ? atomicAdd(a.amb_count + q * NP + half, 1) : n_amb;
-                        if (pos < a.amb_cap) amb_row[pos] = (int32_t)(jb + u);
-                        ++n_amb;
-                    }
+                    am |= (uint32_t)amb << u;
+                }
+                // the chunk's ambiguous columns appended at once (one list reservation per lane and
+                // chunk instead of one atomic round trip per pair), in column order
+                if (am) {
+                    const int cnt = __popc(am);
+                    const int pos0 = a.chunk_block ? atomicAdd(a.amb_count + q * NP + half, cnt) : n_amb;
+                    int pos = pos0;
+                    for (uint32_t m = am; m; m &= m - 1, ++pos)
+                        if (pos < a.amb_cap) amb_row[pos] = (int32_t)(jb + __ffs(m) - 1);
+                    n_amb += cnt;
                 }
             }
             tc_fence_before();
